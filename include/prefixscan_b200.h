@@ -1,0 +1,175 @@
+/*
+ * include/prefixscan_b200.h -- C-ABI of libprefixscan_b200.so, the B200
+ * (sm_100a) prefix-sum path that sits behind the reference package's scan
+ * entry points (/root/reference/pkg/src/prefixscan).
+ *
+ * The reference is pure Python + numba; it has no FFI of its own.  These
+ * exports are the boundary a maintainer binds with ctypes,
+ * one per reference kernel family on the hot path:
+ *
+ *   ps_scan            <- core.py:86-92   _scan_kernel        (+ core.py:118-126 sequential_inclusive_scan)
+ *                         simd.py:75-101  _make_horizontal_kernel (+ simd.py:134-148 horizontal_scan)
+ *                         core.py:109-115 _shift_right_kernel  (fused: exclusive != 0)
+ *   ps_reduce          <- core.py:95-100  _accumulate_kernel   (+ core.py:129-132 sequential_accumulate)
+ *                         simd.py:104-121 _make_simd_accumulate_kernel
+ *   ps_add_offset      <- core.py:103-106 _increment_kernel    (+ core.py:135-138 sequential_increment)
+ *   ps_scan_batched    <- simd.py:164-206 vertical pass kernels (row seeds in, row totals out)
+ *   ps_scan_segmented  <- (no reference kernel; CSR-segment form of the same look-back scan)
+ *   ps_scan_host       <- engine.py:219-248 ScanEngine.run on host buffers (end-to-end call:
+ *                         host->device copy, scan, device->host copy, pipelined)
+ *
+ * Conventions
+ * - extern "C", plain pointers and sizes, no exceptions cross the ABI.
+ * - Every device call is asynchronous on `stream` (a cudaStream_t passed as
+ *   void*; NULL = legacy default stream) except ps_scan_host, which blocks.
+ * - Element counts and leading dimensions are in ELEMENTS.
+ * - The accumulator ("acc") type of a dtype pair: int64 for signed integer
+ *   input, uint64 for uint32 input, double for float32/float64 input.  Seeds,
+ *   totals and deltas are acc-typed 8-byte values.
+ * - Seeds: the carry-in of a scan is  seed_bits (host value, acc bits)
+ *   + sum(seed_terms[0 .. n_seed_terms))  (device array, acc-typed) -- the
+ *   device terms let a multi-GPU carry (allgathered shard totals) flow
+ *   without a host round trip.
+ * - Scratch: look-back descriptors.  Sized by ps_*_scratch_bytes, must be
+ *   ZERO-FILLED when first allocated, and each launch on one scratch buffer
+ *   needs a fresh `epoch` in [1, PS_EPOCH_MAX] strictly greater than the
+ *   previous one (descriptors are epoch-tagged, so no per-call memset).  When
+ *   the epochs run out, zero the buffer again and restart at 1.
+ * - `in == out` (in place) is allowed; partial overlap is not.
+ * - Return 0 on success, a PS_ERR_* (>0) on misuse, or a cudaError_t value
+ *   offset by PS_ERR_CUDA_BASE on a CUDA failure.
+ */
+#ifndef PREFIXSCAN_B200_H
+#define PREFIXSCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype codes (same numbering as oracle/scan_oracle.h) */
+#define PS_DTYPE_INT32 1
+#define PS_DTYPE_INT64 2
+#define PS_DTYPE_UINT32 3
+#define PS_DTYPE_UINT64 4
+#define PS_DTYPE_FLOAT32 5
+#define PS_DTYPE_FLOAT64 6
+
+/* multi-GPU schemes, named after plan.py:24-37 SchemeId */
+#define PS_SCHEME_SCAN_INCREMENT 0   /* scan-then-fixup, 4n bytes  (SCAN_INCREMENT_EQUAL)   */
+#define PS_SCHEME_ACCUMULATE_SCAN 1  /* reduce-then-scan, 3n bytes (ACCUMULATE_SCAN_EQUAL) */
+
+#define PS_EPOCH_MAX 0x3FFFFFFFu
+
+#define PS_OK 0
+#define PS_ERR_DTYPE 1     /* unsupported (dtype_in, dtype_out) pair              */
+#define PS_ERR_ARG 2       /* negative size, NULL buffer, bad leading dimension    */
+#define PS_ERR_SCRATCH 3   /* scratch missing or smaller than ps_*_scratch_bytes   */
+#define PS_ERR_EPOCH 4     /* epoch outside [1, PS_EPOCH_MAX]                      */
+#define PS_ERR_OVERLAP 5   /* in/out partially overlap                             */
+#define PS_ERR_CUDA_BASE 1000
+
+/* Supported (dtype_in -> dtype_out) pairs:
+ *   int32->int32, int32->int64, int64->int64, uint32->uint32, uint32->uint64,
+ *   uint64->uint64, float32->float32, float32->float64, float64->float64 */
+int ps_pair_supported(int dtype_in, int dtype_out);
+
+/* Bytes of look-back scratch for a 1-D scan of n elements. */
+size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out);
+
+/* Inclusive (exclusive == 0) or exclusive scan of in[0..n) into out[0..n).
+ * total_out (device, acc-typed, nullable) receives seed + sum(in).
+ * Replaces core.py:86-92 (+ exclusive: core.py:109-115, whose returned "last"
+ * is *total_out). */
+int ps_scan(const void *in, void *out, int64_t n, int dtype_in, int dtype_out, int exclusive,
+            uint64_t seed_bits, const void *seed_terms, int64_t n_seed_terms, void *total_out,
+            void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream);
+
+/* Bytes of scratch for ps_reduce. */
+size_t ps_reduce_scratch_bytes(int64_t n, int dtype_in);
+
+/* total_out (device, acc-typed) = seed_bits + sum(seed_terms) + sum(in[0..n)).
+ * Read-only on `in`.  Deterministic summation order.  Replaces core.py:95-100. */
+int ps_reduce(const void *in, int64_t n, int dtype_in, uint64_t seed_bits, const void *seed_terms,
+              int64_t n_seed_terms, void *total_out, void *scratch, size_t scratch_bytes,
+              void *stream);
+
+/* buf[i] = buf[i] + delta, delta = delta_bits + sum(delta_terms), computed in
+ * the acc type and stored back in the element type.  Replaces core.py:103-106. */
+int ps_add_offset(void *buf, int64_t n, int dtype, uint64_t delta_bits, const void *delta_terms,
+                  int64_t n_delta_terms, void *stream);
+
+/* Bytes of scratch for ps_scan_batched. */
+size_t ps_scan_batched_scratch_bytes(int64_t rows, int64_t cols, int dtype_in, int dtype_out);
+
+/* rows independent scans: out[r*ld_out + c] = row_seeds[r] + sum_{c'<=c} in[r*ld_in + c']
+ * (exclusive: c' < c).  row_seeds / row_totals: device, acc-typed, nullable. */
+int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in,
+                    int64_t ld_out, int dtype_in, int dtype_out, int exclusive,
+                    const void *row_seeds, void *row_totals, void *scratch, size_t scratch_bytes,
+                    uint32_t epoch, void *stream);
+
+/* Bytes of scratch for ps_scan_segmented. */
+size_t ps_scan_segmented_scratch_bytes(int64_t n, int dtype_in, int dtype_out);
+
+/* Segmented scan over CSR segments of one contiguous buffer: segment s is
+ * in[seg_offsets[s] .. seg_offsets[s+1]), seg_offsets (device int64, nseg+1
+ * entries, non-decreasing, seg_offsets[0] == 0, seg_offsets[nseg] == n).
+ * Every segment restarts at zero; seg_totals (device acc-typed, nullable)
+ * receives each segment's sum. */
+int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_offsets,
+                      int64_t nseg, int dtype_in, int dtype_out, int exclusive, void *seg_totals,
+                      void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream);
+
+/* Bytes of scratch for ps_shift_right. */
+size_t ps_shift_right_scratch_bytes(int64_t n, int dtype);
+
+/* out[0] = identity, out[i] = in[i-1]; *last_out (device, element-typed,
+ * nullable) = in[n-1].  in == out allowed.  Replaces exclusive_from_inclusive
+ * (core.py:141-151 / _shift_right_kernel core.py:109-115); the fused form is
+ * ps_scan(..., exclusive=1, ...). */
+int ps_shift_right(const void *in, void *out, int64_t n, int dtype, uint64_t identity_bits, void *last_out,
+                   void *scratch, size_t scratch_bytes, void *stream);
+
+/* row_totals[r] (device, acc-typed) = sum(in[r*ld_in .. r*ld_in+cols)).  Read-only.
+ * Replaces simd.py:178-186 _vertical_pass1_accumulate. */
+int ps_reduce_batched(const void *in, int64_t rows, int64_t cols, int64_t ld_in, int dtype_in, void *row_totals,
+                      void *stream);
+
+/* buf[r*ld + c] += row_deltas[r] (device, acc-typed).  rows <= 65535.
+ * Replaces simd.py:189-195 _vertical_pass2_increment. */
+int ps_add_offset_batched(void *buf, int64_t rows, int64_t cols, int64_t ld, int dtype, const void *row_deltas,
+                          void *stream);
+
+/* *total_out (device uint64) = seed + sum over w-blocks of (block sum mod 2^32)
+ * + the scalar tail: the total the reference's horizontal kernel returns for
+ * uint32 data (simd.py:84-99).  Read-only on `in`. */
+int ps_reduce_wrapped_blocks(const void *in, int64_t n, int w, uint64_t seed_bits, void *total_out, void *stream);
+
+/* Device workspace for ps_scan_host with the given chunk size. */
+size_t ps_scan_host_workspace_bytes(int64_t chunk_elems, int dtype_in, int dtype_out);
+
+/* Number of epochs ps_scan_host consumes (one per chunk). */
+int64_t ps_scan_host_epochs(int64_t n, int64_t chunk_elems);
+
+/* End-to-end scan of HOST buffers (pinned for full speed): chunked pipeline of
+ * H2D copy -> look-back scan seeded by the previous chunk's total -> D2H copy
+ * over three CUDA streams.  Blocks until out_host and *total_host (acc-typed,
+ * host, nullable) are written.  Epochs epoch .. epoch+ps_scan_host_epochs-1
+ * are used on the scratch inside `workspace` (zero-filled when allocated). */
+int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, int dtype_out,
+                 int exclusive, uint64_t seed_bits, void *total_host, void *workspace,
+                 size_t workspace_bytes, int64_t chunk_elems, uint32_t epoch, void *stream);
+
+/* Human-readable text for a return code. */
+const char *ps_error_string(int code);
+
+/* ABI version (major*100 + minor). */
+int ps_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PREFIXSCAN_B200_H */

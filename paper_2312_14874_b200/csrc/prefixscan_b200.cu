@@ -1,0 +1,525 @@
+// prefixscan_b200.cu -- C-ABI of libprefixscan_b200.so (see include/prefixscan_b200.h).
+//
+// Host side of the sm_100a scan path: argument validation (the reference's
+// ValueError cases map to PS_ERR_*), dtype-pair dispatch, tile geometry,
+// scratch carving, launches, and the pipelined host-buffer entry point.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/prefixscan_b200.h"
+#include "scan_kernels.cuh"
+#include "segmented.cuh"
+#include "aux_kernels.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int SCAN_WARPS = 8;
+constexpr int SCAN_ROWS = 4;
+constexpr int REDUCE_THREADS = 512;
+
+template <typename TIn> constexpr int64_t tile_elems() {
+    return (int64_t)SCAN_WARPS * SCAN_ROWS * 32 * (32 / sizeof(TIn));
+}
+
+size_t dsize(int dt) {
+    switch (dt) {
+        case PS_DTYPE_INT32: case PS_DTYPE_UINT32: case PS_DTYPE_FLOAT32: return 4;
+        case PS_DTYPE_INT64: case PS_DTYPE_UINT64: case PS_DTYPE_FLOAT64: return 8;
+        default: return 0;
+    }
+}
+
+bool pair_ok(int i, int o) {
+    switch (i) {
+        case PS_DTYPE_INT32: return o == PS_DTYPE_INT32 || o == PS_DTYPE_INT64;
+        case PS_DTYPE_INT64: return o == PS_DTYPE_INT64;
+        case PS_DTYPE_UINT32: return o == PS_DTYPE_UINT32 || o == PS_DTYPE_UINT64;
+        case PS_DTYPE_UINT64: return o == PS_DTYPE_UINT64;
+        case PS_DTYPE_FLOAT32: return o == PS_DTYPE_FLOAT32 || o == PS_DTYPE_FLOAT64;
+        case PS_DTYPE_FLOAT64: return o == PS_DTYPE_FLOAT64;
+        default: return false;
+    }
+}
+
+int64_t tile_of_dtype(int dt) { return (int64_t)SCAN_WARPS * SCAN_ROWS * 32 * (int64_t)(32 / (dsize(dt) ? dsize(dt) : 4)); }
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t desc_bytes(int64_t tiles) {
+    return align_up((size_t)tiles * 4, 256) + 2 * align_up((size_t)tiles * 8, 256);
+}
+
+Desc carve_desc(void *scratch, int64_t tiles) {
+    char *p = static_cast<char *>(scratch);
+    Desc d;
+    d.flags = reinterpret_cast<uint32_t *>(p);
+    p += align_up((size_t)tiles * 4, 256);
+    d.agg = reinterpret_cast<uint64_t *>(p);
+    p += align_up((size_t)tiles * 8, 256);
+    d.incl = reinterpret_cast<uint64_t *>(p);
+    return d;
+}
+
+int cuda_rc(cudaError_t e) { return e == cudaSuccess ? PS_OK : PS_ERR_CUDA_BASE + (int)e; }
+
+int launch_rc() { return cuda_rc(cudaGetLastError()); }
+
+bool overlaps_partially(const void *a, size_t abytes, const void *b, size_t bbytes) {
+    if (a == b) return false;
+    const uintptr_t a0 = (uintptr_t)a, a1 = a0 + abytes, b0 = (uintptr_t)b, b1 = b0 + bbytes;
+    return a0 < b1 && b0 < a1;
+}
+
+// ---- scan (1-D and batched share one kernel) ----------------------------------------------
+template <typename TIn, typename TOut>
+int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
+                int exclusive, uint64_t seed_bits, const void *seed_terms, int64_t n_seed_terms,
+                void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s) {
+    constexpr int64_t TILE = tile_elems<TIn>();
+    ScanArgs a{};
+    a.in = in;
+    a.out = out;
+    a.rows = rows;
+    a.cols = cols;
+    a.ld_in = ld_in;
+    a.ld_out = ld_out;
+    a.seed_bits = seed_bits;
+    a.seed_terms = seed_terms;
+    a.n_seed_terms = n_seed_terms;
+    a.totals = totals;
+    a.epoch = epoch;
+    a.exclusive = exclusive;
+    // alignment: tiles start on 32-byte boundaries of the input; the output
+    // must sit at the same element phase for the 256-bit store path
+    const uintptr_t ain = (uintptr_t)in % 32;
+    int64_t lead = (ain % sizeof(TIn)) ? -1 : (int64_t)(ain / sizeof(TIn));
+    bool vec = lead >= 0 && ((uintptr_t)out % 32) == (uintptr_t)((lead * sizeof(TOut)) % 32) &&
+               (uintptr_t)out % sizeof(TOut) == 0;
+    if (rows > 1) vec = vec && (ld_in * sizeof(TIn)) % 32 == 0 && (ld_out * sizeof(TOut)) % 32 == 0;
+    if (vec && lead * (int64_t)sizeof(TOut) >= 32) vec = false;
+    a.vec_ok = vec;
+    a.lead = vec ? lead : 0;
+    a.tiles_per_row = (a.lead + cols + TILE - 1) / TILE;
+    const int64_t tiles = rows * a.tiles_per_row;
+    if (tiles > 0x7fffffffLL) return PS_ERR_ARG;
+    if (a.tiles_per_row > 1) {
+        if (!scratch || scratch_bytes < desc_bytes(tiles)) return PS_ERR_SCRATCH;
+        a.desc = carve_desc(scratch, tiles);
+    }
+    scan_tiles_kernel<TIn, TOut, SCAN_WARPS, SCAN_ROWS><<<(unsigned)tiles, SCAN_WARPS * 32, 0, s>>>(a);
+    return launch_rc();
+}
+
+template <typename A> __global__ void fill_seed_kernel(A *dst, int64_t count, uint64_t seed_bits, const void *terms,
+                                                       int64_t n_terms, int per_row) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    A v = acc_from_bits<A>(seed_bits);
+    if (terms) {
+        const A *t = reinterpret_cast<const A *>(terms);
+        if (per_row) v += t[i];
+        else for (int64_t k = 0; k < n_terms; ++k) v += t[k];
+    }
+    dst[i] = v;
+}
+
+#define PS_DISPATCH_PAIR(din, dout, CALL)                                                      \
+    do {                                                                                        \
+        if (din == PS_DTYPE_INT32 && dout == PS_DTYPE_INT32) { CALL(int32_t, int32_t); }        \
+        else if (din == PS_DTYPE_INT32 && dout == PS_DTYPE_INT64) { CALL(int32_t, int64_t); }   \
+        else if (din == PS_DTYPE_INT64 && dout == PS_DTYPE_INT64) { CALL(int64_t, int64_t); }   \
+        else if (din == PS_DTYPE_UINT32 && dout == PS_DTYPE_UINT32) { CALL(uint32_t, uint32_t); } \
+        else if (din == PS_DTYPE_UINT32 && dout == PS_DTYPE_UINT64) { CALL(uint32_t, uint64_t); } \
+        else if (din == PS_DTYPE_UINT64 && dout == PS_DTYPE_UINT64) { CALL(uint64_t, uint64_t); } \
+        else if (din == PS_DTYPE_FLOAT32 && dout == PS_DTYPE_FLOAT32) { CALL(float, float); }   \
+        else if (din == PS_DTYPE_FLOAT32 && dout == PS_DTYPE_FLOAT64) { CALL(float, double); }  \
+        else if (din == PS_DTYPE_FLOAT64 && dout == PS_DTYPE_FLOAT64) { CALL(double, double); } \
+        else return PS_ERR_DTYPE;                                                               \
+    } while (0)
+
+#define PS_DISPATCH_ONE(dt, CALL)                                        \
+    do {                                                                  \
+        switch (dt) {                                                     \
+            case PS_DTYPE_INT32: CALL(int32_t); break;                    \
+            case PS_DTYPE_INT64: CALL(int64_t); break;                    \
+            case PS_DTYPE_UINT32: CALL(uint32_t); break;                  \
+            case PS_DTYPE_UINT64: CALL(uint64_t); break;                  \
+            case PS_DTYPE_FLOAT32: CALL(float); break;                    \
+            case PS_DTYPE_FLOAT64: CALL(double); break;                   \
+            default: return PS_ERR_DTYPE;                                 \
+        }                                                                 \
+    } while (0)
+
+// Empty input: totals (if requested) still receive the seed (core.py:152-156:
+// a zero-length span returns the offset).
+int write_seed_only(int din, void *totals, int64_t count, uint64_t seed_bits, const void *terms, int64_t n_terms,
+                    int per_row, cudaStream_t s) {
+    if (!totals || count == 0) return PS_OK;
+    const unsigned blocks = (unsigned)((count + 255) / 256);
+#define FILL(T)                                                                                     \
+    fill_seed_kernel<typename AccOf<T>::type><<<blocks, 256, 0, s>>>(                               \
+        reinterpret_cast<typename AccOf<T>::type *>(totals), count, seed_bits, terms, n_terms, per_row)
+    PS_DISPATCH_ONE(din, FILL);
+#undef FILL
+    return launch_rc();
+}
+
+// ---- host-buffer pipeline: per-device helper streams/events ---------------------------------
+constexpr int NSLOT = 3;
+struct HostPipe {
+    bool ready = false;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr, h2d_done[NSLOT], comp_done[NSLOT], d2h_done[NSLOT], end_d2h = nullptr;
+};
+std::mutex g_pipe_mu;
+HostPipe g_pipes[64];
+
+int get_pipe(HostPipe **out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_rc(e);
+    if (dev < 0 || dev >= 64) return PS_ERR_ARG;
+    std::lock_guard<std::mutex> g(g_pipe_mu);
+    HostPipe &p = g_pipes[dev];
+    if (!p.ready) {
+        if ((e = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking)) != cudaSuccess) return cuda_rc(e);
+        if ((e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking)) != cudaSuccess) return cuda_rc(e);
+        cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&p.end_d2h, cudaEventDisableTiming);
+        for (int i = 0; i < NSLOT; ++i) {
+            cudaEventCreateWithFlags(&p.h2d_done[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&p.comp_done[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&p.d2h_done[i], cudaEventDisableTiming);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_rc(e);
+        p.ready = true;
+    }
+    *out = &p;
+    return PS_OK;
+}
+
+struct HostLayout {
+    size_t in_slot, out_slot, scratch, total;  // byte sizes
+    size_t off_in, off_out, off_scratch, off_carry;
+};
+
+HostLayout host_layout(int64_t chunk, int din, int dout) {
+    HostLayout L{};
+    L.in_slot = align_up((size_t)chunk * dsize(din), 256);
+    L.out_slot = align_up((size_t)chunk * dsize(dout), 256);
+    const int64_t tiles = (chunk + tile_of_dtype(din) - 1) / tile_of_dtype(din) + 1;
+    L.scratch = align_up(desc_bytes(tiles), 256);
+    L.off_in = 0;
+    L.off_out = L.off_in + NSLOT * L.in_slot;
+    L.off_scratch = L.off_out + NSLOT * L.out_slot;
+    L.off_carry = L.off_scratch + L.scratch;
+    L.total = L.off_carry + 256;
+    return L;
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+int ps_version(void) { return 100; }
+
+int ps_pair_supported(int dtype_in, int dtype_out) { return pair_ok(dtype_in, dtype_out) ? 1 : 0; }
+
+const char *ps_error_string(int code) {
+    switch (code) {
+        case PS_OK: return "ok";
+        case PS_ERR_DTYPE: return "unsupported dtype pair";
+        case PS_ERR_ARG: return "invalid argument (size, pointer or leading dimension)";
+        case PS_ERR_SCRATCH: return "scratch buffer missing or too small";
+        case PS_ERR_EPOCH: return "epoch outside [1, PS_EPOCH_MAX]";
+        case PS_ERR_OVERLAP: return "input and output partially overlap";
+        default:
+            if (code >= PS_ERR_CUDA_BASE) return cudaGetErrorString((cudaError_t)(code - PS_ERR_CUDA_BASE));
+            return "unknown error";
+    }
+}
+
+size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
+    if (!pair_ok(dtype_in, dtype_out) || n < 0) return 0;
+    const int64_t tile = tile_of_dtype(dtype_in);
+    return desc_bytes((n + tile - 1) / tile + 1);  // +1: a misaligned start can add a tile
+}
+
+int ps_scan(const void *in, void *out, int64_t n, int dtype_in, int dtype_out, int exclusive, uint64_t seed_bits,
+            const void *seed_terms, int64_t n_seed_terms, void *total_out, void *scratch, size_t scratch_bytes,
+            uint32_t epoch, void *stream) {
+    if (!pair_ok(dtype_in, dtype_out)) return PS_ERR_DTYPE;
+    if (n < 0 || n_seed_terms < 0 || (n > 0 && (!in || !out)) || (seed_terms == nullptr && n_seed_terms > 0))
+        return PS_ERR_ARG;
+    if (epoch == 0 || epoch > PS_EPOCH_MAX) return PS_ERR_EPOCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) return write_seed_only(dtype_in, total_out, 1, seed_bits, seed_terms, n_seed_terms, 0, s);
+    if (overlaps_partially(in, (size_t)n * dsize(dtype_in), out, (size_t)n * dsize(dtype_out))) return PS_ERR_OVERLAP;
+    if (in == out && dsize(dtype_in) != dsize(dtype_out)) return PS_ERR_OVERLAP;
+#define CALL(TI, TO)                                                                                          \
+    return launch_scan<TI, TO>(in, out, 1, n, n, n, exclusive, seed_bits, seed_terms, n_seed_terms, total_out, \
+                               scratch, scratch_bytes, epoch, s)
+    PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);
+#undef CALL
+}
+
+size_t ps_scan_batched_scratch_bytes(int64_t rows, int64_t cols, int dtype_in, int dtype_out) {
+    if (!pair_ok(dtype_in, dtype_out) || rows < 0 || cols < 0) return 0;
+    const int64_t tile = tile_of_dtype(dtype_in);
+    return desc_bytes(rows * ((cols + tile - 1) / tile + 1));
+}
+
+int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
+                    int dtype_in, int dtype_out, int exclusive, const void *row_seeds, void *row_totals,
+                    void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream) {
+    if (!pair_ok(dtype_in, dtype_out)) return PS_ERR_DTYPE;
+    if (rows < 0 || cols < 0 || ld_in < cols || ld_out < cols) return PS_ERR_ARG;
+    if (epoch == 0 || epoch > PS_EPOCH_MAX) return PS_ERR_EPOCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (rows == 0) return PS_OK;
+    if (cols == 0) return write_seed_only(dtype_in, row_totals, rows, 0, row_seeds, rows, 1, s);
+    if (!in || !out) return PS_ERR_ARG;
+    if (in == out && (dsize(dtype_in) != dsize(dtype_out) || ld_in != ld_out)) return PS_ERR_OVERLAP;
+    if (rows == 1) ld_in = ld_out = cols;
+#define CALL(TI, TO)                                                                                            \
+    return launch_scan<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, 0, row_seeds, row_seeds ? rows : 0, \
+                               row_totals, scratch, scratch_bytes, epoch, s)
+    PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);
+#undef CALL
+}
+
+size_t ps_reduce_scratch_bytes(int64_t n, int dtype_in) {
+    (void)n;
+    if (!dsize(dtype_in)) return 0;
+    return 256 + 8 * 4096;  // ticket + up to 4096 CTA partials
+}
+
+int ps_reduce(const void *in, int64_t n, int dtype_in, uint64_t seed_bits, const void *seed_terms,
+              int64_t n_seed_terms, void *total_out, void *scratch, size_t scratch_bytes, void *stream) {
+    if (!dsize(dtype_in)) return PS_ERR_DTYPE;
+    if (n < 0 || !total_out || (n > 0 && !in)) return PS_ERR_ARG;
+    if (!scratch || scratch_bytes < ps_reduce_scratch_bytes(n, dtype_in)) return PS_ERR_SCRATCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t vec = 32 / (int64_t)dsize(dtype_in);
+    int64_t want = (n / vec + REDUCE_THREADS * 4 - 1) / (REDUCE_THREADS * 4);
+    int64_t grid = want < (int64_t)sms * 4 ? want : (int64_t)sms * 4;
+    if (grid < 1) grid = 1;
+    ReduceArgs a{};
+    a.in = in;
+    a.n = n;
+    const uintptr_t ain = (uintptr_t)in % 32;
+    a.lead = (ain % dsize(dtype_in)) ? n : (int64_t)(((32 - ain) % 32) / dsize(dtype_in));
+    a.seed_bits = seed_bits;
+    a.seed_terms = seed_terms;
+    a.n_seed_terms = n_seed_terms;
+    a.total = total_out;
+    a.ticket = static_cast<uint32_t *>(scratch);
+    a.partials = reinterpret_cast<uint64_t *>(static_cast<char *>(scratch) + 256);
+#define CALL(T) reduce_kernel<T, REDUCE_THREADS><<<(unsigned)grid, REDUCE_THREADS, 0, s>>>(a)
+    PS_DISPATCH_ONE(dtype_in, CALL);
+#undef CALL
+    return launch_rc();
+}
+
+int ps_add_offset(void *buf, int64_t n, int dtype, uint64_t delta_bits, const void *delta_terms,
+                  int64_t n_delta_terms, void *stream) {
+    if (!dsize(dtype)) return PS_ERR_DTYPE;
+    if (n < 0 || (n > 0 && !buf) || n_delta_terms < 0) return PS_ERR_ARG;
+    if (n == 0) return PS_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uintptr_t ab = (uintptr_t)buf % 32;
+    const int64_t lead = (ab % dsize(dtype)) ? n : (int64_t)(((32 - ab) % 32) / dsize(dtype));
+    const int64_t vec = 32 / (int64_t)dsize(dtype);
+    int64_t want = (n / vec + 255) / 256;
+    int64_t grid = want < (int64_t)sms * 8 ? want : (int64_t)sms * 8;
+    if (grid < 1) grid = 1;
+#define CALL(T)                                                                                          \
+    add_offset_kernel<T><<<(unsigned)grid, 256, 0, s>>>(static_cast<T *>(buf), n, lead, delta_bits, delta_terms, \
+                                                        n_delta_terms)
+    PS_DISPATCH_ONE(dtype, CALL);
+#undef CALL
+    return launch_rc();
+}
+
+size_t ps_scan_segmented_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
+    if (!pair_ok(dtype_in, dtype_out) || n < 0) return 0;
+    return seg_scratch_bytes(n, (int)dsize(dtype_in));
+}
+
+int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_offsets, int64_t nseg,
+                      int dtype_in, int dtype_out, int exclusive, void *seg_totals, void *scratch,
+                      size_t scratch_bytes, uint32_t epoch, void *stream) {
+    if (!pair_ok(dtype_in, dtype_out)) return PS_ERR_DTYPE;
+    if (n < 0 || nseg < 0 || (nseg > 0 && !seg_offsets) || (n > 0 && (!in || !out))) return PS_ERR_ARG;
+    if (epoch == 0 || epoch > PS_EPOCH_MAX) return PS_ERR_EPOCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (nseg == 0) return PS_OK;
+    if (seg_totals) {
+        cudaError_t e = cudaMemsetAsync(seg_totals, 0, (size_t)nseg * 8, s);
+        if (e != cudaSuccess) return cuda_rc(e);
+    }
+    if (n == 0) return PS_OK;
+    if (overlaps_partially(in, (size_t)n * dsize(dtype_in), out, (size_t)n * dsize(dtype_out))) return PS_ERR_OVERLAP;
+    if (in == out && dsize(dtype_in) != dsize(dtype_out)) return PS_ERR_OVERLAP;
+    if (!scratch || scratch_bytes < seg_scratch_bytes(n, (int)dsize(dtype_in))) return PS_ERR_SCRATCH;
+#define CALL(TI, TO) \
+    return launch_segmented<TI, TO>(in, out, n, seg_offsets, nseg, exclusive, seg_totals, scratch, epoch, s)
+    PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);
+#undef CALL
+}
+
+size_t ps_shift_right_scratch_bytes(int64_t n, int dtype) {
+    if (!dsize(dtype) || n < 0) return 0;
+    return align_up((size_t)((n + SHIFT_TILE - 1) / SHIFT_TILE + 1) * 8, 256);
+}
+
+int ps_shift_right(const void *in, void *out, int64_t n, int dtype, uint64_t identity_bits, void *last_out,
+                   void *scratch, size_t scratch_bytes, void *stream) {
+    if (!dsize(dtype)) return PS_ERR_DTYPE;
+    if (n < 0 || (n > 0 && (!in || !out))) return PS_ERR_ARG;
+    if (n == 0) return PS_OK;
+    if (overlaps_partially(in, (size_t)n * dsize(dtype), out, (size_t)n * dsize(dtype))) return PS_ERR_OVERLAP;
+    if (!scratch || scratch_bytes < ps_shift_right_scratch_bytes(n, dtype)) return PS_ERR_SCRATCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t tiles = (n + SHIFT_TILE - 1) / SHIFT_TILE;
+    if (tiles > 0x7fffffffLL) return PS_ERR_ARG;
+#define CALL(T)                                                                                              \
+    do {                                                                                                     \
+        shift_gather_kernel<T><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(                              \
+            static_cast<const T *>(in), n, tiles, static_cast<T *>(scratch), static_cast<T *>(last_out));     \
+        shift_tiles_kernel<T><<<(unsigned)tiles, SHIFT_THREADS, 0, s>>>(                                     \
+            static_cast<const T *>(in), static_cast<T *>(out), n, static_cast<const T *>(scratch), identity_bits); \
+    } while (0)
+    PS_DISPATCH_ONE(dtype, CALL);
+#undef CALL
+    return launch_rc();
+}
+
+int ps_reduce_batched(const void *in, int64_t rows, int64_t cols, int64_t ld_in, int dtype_in, void *row_totals,
+                      void *stream) {
+    if (!dsize(dtype_in)) return PS_ERR_DTYPE;
+    if (rows < 0 || cols < 0 || ld_in < cols || (rows > 0 && !row_totals) || (rows > 0 && cols > 0 && !in))
+        return PS_ERR_ARG;
+    if (rows == 0) return PS_OK;
+    if (rows > 0x7fffffffLL) return PS_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+#define CALL(T) \
+    reduce_rows_kernel<T, 256><<<(unsigned)rows, 256, 0, s>>>(static_cast<const T *>(in), cols, ld_in, row_totals)
+    PS_DISPATCH_ONE(dtype_in, CALL);
+#undef CALL
+    return launch_rc();
+}
+
+int ps_add_offset_batched(void *buf, int64_t rows, int64_t cols, int64_t ld, int dtype, const void *row_deltas,
+                          void *stream) {
+    if (!dsize(dtype)) return PS_ERR_DTYPE;
+    if (rows < 0 || cols < 0 || ld < cols || (rows > 0 && cols > 0 && (!buf || !row_deltas))) return PS_ERR_ARG;
+    if (rows == 0 || cols == 0) return PS_OK;
+    if (rows > 65535) return PS_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int64_t gx = (cols + 255) / 256;
+    if (gx > 1024) gx = 1024;
+    dim3 grid((unsigned)gx, (unsigned)rows);
+#define CALL(T) add_rows_kernel<T><<<grid, 256, 0, s>>>(static_cast<T *>(buf), cols, ld, row_deltas)
+    PS_DISPATCH_ONE(dtype, CALL);
+#undef CALL
+    return launch_rc();
+}
+
+int ps_reduce_wrapped_blocks(const void *in, int64_t n, int w, uint64_t seed_bits, void *total_out, void *stream) {
+    if (n < 0 || w < 1 || !total_out || (n > 0 && !in)) return PS_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    fill_seed_kernel<uint64_t><<<1, 32, 0, s>>>(static_cast<uint64_t *>(total_out), 1, seed_bits, nullptr, 0, 0);
+    if (n > 0) {
+        int64_t grid = (n / w + 255) / 256;
+        if (grid > 148 * 8) grid = 148 * 8;
+        if (grid < 1) grid = 1;
+        wrapped_block_total_kernel<<<(unsigned)grid, 256, 0, s>>>(static_cast<const uint32_t *>(in), n, w,
+                                                                  static_cast<unsigned long long *>(total_out));
+    }
+    return launch_rc();
+}
+
+size_t ps_scan_host_workspace_bytes(int64_t chunk_elems, int dtype_in, int dtype_out) {
+    if (!pair_ok(dtype_in, dtype_out) || chunk_elems <= 0) return 0;
+    return host_layout(chunk_elems, dtype_in, dtype_out).total;
+}
+
+int64_t ps_scan_host_epochs(int64_t n, int64_t chunk_elems) {
+    if (n <= 0 || chunk_elems <= 0) return 1;
+    return (n + chunk_elems - 1) / chunk_elems;
+}
+
+int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, int dtype_out, int exclusive,
+                 uint64_t seed_bits, void *total_host, void *workspace, size_t workspace_bytes, int64_t chunk_elems,
+                 uint32_t epoch, void *stream) {
+    if (!pair_ok(dtype_in, dtype_out)) return PS_ERR_DTYPE;
+    if (n < 0 || chunk_elems <= 0 || (n > 0 && (!in_host || !out_host))) return PS_ERR_ARG;
+    const int64_t nchunks = ps_scan_host_epochs(n, chunk_elems);
+    if (epoch == 0 || (uint64_t)epoch + (uint64_t)nchunks - 1 > PS_EPOCH_MAX) return PS_ERR_EPOCH;
+    const HostLayout L = host_layout(chunk_elems, dtype_in, dtype_out);
+    if (!workspace || workspace_bytes < L.total) return PS_ERR_SCRATCH;
+    cudaStream_t comp = static_cast<cudaStream_t>(stream);
+    char *ws = static_cast<char *>(workspace);
+    void *carry = ws + L.off_carry;
+    void *scratch = ws + L.off_scratch;
+    if (n == 0) {
+        if (total_host) std::memcpy(total_host, &seed_bits, 8);
+        return PS_OK;
+    }
+    HostPipe *P = nullptr;
+    int rc = get_pipe(&P);
+    if (rc) return rc;
+    cudaError_t e;
+    // helper streams start after everything already queued on the caller stream
+    if ((e = cudaEventRecord(P->start, comp)) != cudaSuccess) return cuda_rc(e);
+    cudaStreamWaitEvent(P->h2d, P->start, 0);
+    cudaStreamWaitEvent(P->d2h, P->start, 0);
+    const size_t bi = dsize(dtype_in), bo = dsize(dtype_out);
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int slot = (int)(k % NSLOT);
+        const int64_t off = k * chunk_elems;
+        const int64_t len = (n - off) < chunk_elems ? (n - off) : chunk_elems;
+        void *din = ws + L.off_in + slot * L.in_slot;
+        void *dout = ws + L.off_out + slot * L.out_slot;
+        if (k >= NSLOT) cudaStreamWaitEvent(P->h2d, P->d2h_done[slot], 0);
+        e = cudaMemcpyAsync(din, static_cast<const char *>(in_host) + off * bi, (size_t)len * bi,
+                            cudaMemcpyHostToDevice, P->h2d);
+        if (e != cudaSuccess) return cuda_rc(e);
+        cudaEventRecord(P->h2d_done[slot], P->h2d);
+        cudaStreamWaitEvent(comp, P->h2d_done[slot], 0);
+        rc = ps_scan(din, dout, len, dtype_in, dtype_out, exclusive, k == 0 ? seed_bits : 0,
+                     k == 0 ? nullptr : carry, k == 0 ? 0 : 1, carry, scratch, L.scratch, epoch + (uint32_t)k, comp);
+        if (rc) return rc;
+        cudaEventRecord(P->comp_done[slot], comp);
+        cudaStreamWaitEvent(P->d2h, P->comp_done[slot], 0);
+        e = cudaMemcpyAsync(static_cast<char *>(out_host) + off * bo, dout, (size_t)len * bo,
+                            cudaMemcpyDeviceToHost, P->d2h);
+        if (e != cudaSuccess) return cuda_rc(e);
+        cudaEventRecord(P->d2h_done[slot], P->d2h);
+    }
+    if (total_host) {
+        e = cudaMemcpyAsync(total_host, carry, 8, cudaMemcpyDeviceToHost, comp);
+        if (e != cudaSuccess) return cuda_rc(e);
+    }
+    // the caller stream owns the workspace again only after the last D2H
+    cudaEventRecord(P->end_d2h, P->d2h);
+    cudaStreamWaitEvent(comp, P->end_d2h, 0);
+    e = cudaStreamSynchronize(comp);
+    return cuda_rc(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// scan_device.cuh -- device building blocks of the sm_100a look-back scan.
+//
+// What the reference does on the CPU, and what each piece here replaces:
+//   * simd.py:55-72 vector_inclusive_scan: log2(w) shift-add rounds over w
+//     lanes  ->  warp_inclusive_scan: 5 __shfl_up_sync rounds over 32 lanes.
+//   * simd.py:75-101 horizontal kernel: block scan + running carry  ->  one
+//     tile per CTA, carry obtained by decoupled look-back over predecessor
+//     tiles' published aggregates / inclusive prefixes (replaces the
+//     engine's barrier + ledger fold, engine.py:314, :329-331).
+//   * core.py:40-48 accumulator typing: elements are widened to the acc type
+//     (int64 / uint64 / double) before any addition.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ps {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---- accumulator traits ------------------------------------------------------
+template <typename T> struct AccOf;
+template <> struct AccOf<int32_t> { using type = int64_t; };
+template <> struct AccOf<int64_t> { using type = int64_t; };
+template <> struct AccOf<uint32_t> { using type = uint64_t; };
+template <> struct AccOf<uint64_t> { using type = uint64_t; };
+template <> struct AccOf<float> { using type = double; };
+template <> struct AccOf<double> { using type = double; };
+
+template <typename A> __device__ __forceinline__ A acc_from_bits(uint64_t b) {
+    if constexpr (sizeof(A) == 8 && (A)0.5 != (A)0) return __longlong_as_double((long long)b);
+    else return (A)b;
+}
+template <typename A> __device__ __forceinline__ uint64_t acc_to_bits(A v) {
+    if constexpr ((A)0.5 != (A)0) return (uint64_t)__double_as_longlong(v);
+    else return (uint64_t)v;
+}
+
+// ---- memory-model primitives for the tile descriptors --------------------------
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---- 256-bit streaming global access (LDG.E.256 / STG.E.256 on sm_100a) -------
+struct alignas(32) V256 {
+    uint64_t w[4];
+};
+__device__ __forceinline__ V256 ldg256_stream(const void *p) {
+    V256 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void stg256_stream(void *p, const V256 &v) {
+    asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v.w[0]),
+                 "l"(v.w[1]), "l"(v.w[2]), "l"(v.w[3])
+                 : "memory");
+}
+
+// ---- warp primitives ------------------------------------------------------------
+template <typename A> __device__ __forceinline__ A shfl_up(A v, int d) {
+    return __shfl_up_sync(FULL, v, d);
+}
+template <typename A> __device__ __forceinline__ A shfl_idx(A v, int src) {
+    return __shfl_sync(FULL, v, src);
+}
+template <typename A> __device__ __forceinline__ A warp_sum(A v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+
+// Descriptor status values (low 2 bits of the epoch-tagged flag word).
+constexpr uint32_t ST_A = 1;  // aggregate published
+constexpr uint32_t ST_P = 2;  // inclusive prefix published
+
+struct Desc {
+    uint32_t *flags;  // (epoch << 2) | status, one per tile
+    uint64_t *agg;    // tile aggregate (acc bits)
+    uint64_t *incl;   // tile inclusive prefix (acc bits)
+};
+
+__device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t epoch, uint32_t st,
+                                        uint64_t bits) {
+    st_relaxed_u64(st == ST_P ? d.incl + tile : d.agg + tile, bits);
+    st_release_u32(d.flags + tile, (epoch << 2) | st);
+}
+
+// Warp-parallel decoupled look-back (one full warp).  Returns the exclusive
+// prefix of `tile` within its segment [head, ...).  Lane j inspects tile
+// base-j; the window slides back 32 tiles until a P descriptor is seen.
+// Tiles before `head` are treated as P with value 0 (the head tile always
+// publishes P directly, so the scan never needs to read past it).
+template <typename A>
+__device__ A lookback(const Desc &d, int64_t tile, int64_t head, uint32_t epoch, int lane) {
+    const uint32_t want = epoch << 2;
+    A excl = (A)0;
+    int64_t base = tile - 1;
+    while (true) {
+        const int64_t p = base - lane;
+        const bool live = p >= head;
+        uint32_t f = live ? ld_acquire_u32(d.flags + p) : (want | ST_P);
+        int spins = 0;
+        while (__any_sync(FULL, (f & ~3u) != want || (f & 3u) == 0)) {
+            if (++spins > 4) __nanosleep(spins > 64 ? 256 : 32);
+            if ((f & ~3u) != want || (f & 3u) == 0) f = ld_acquire_u32(d.flags + p);
+        }
+        const unsigned pmask = __ballot_sync(FULL, (f & 3u) == ST_P);
+        const int first_p = pmask ? __ffs(pmask) - 1 : 32;
+        A v = (A)0;
+        if (live) {
+            if (lane < first_p) v = acc_from_bits<A>(ld_relaxed_u64(d.agg + p));
+            else if (lane == first_p) v = acc_from_bits<A>(ld_relaxed_u64(d.incl + p));
+        }
+        excl += warp_sum(v);
+        if (pmask) return excl;
+        base -= 32;
+    }
+}
+
+}  // namespace ps

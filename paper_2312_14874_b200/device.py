@@ -1,0 +1,378 @@
+"""Device-level scan API over CUDA tensors (the layer the reference-shaped
+modules core / simd / engine call).
+
+Every function here is one or two launches of the sm_100a library on the
+caller's current CUDA stream and returns without synchronising; totals come
+back as 1-element device tensors in the accumulator dtype (int64 for signed
+input, uint64 for uint32 input, float64 for floating input -- the
+accumulator typing of core.py:40-48, with signed integers kept exact instead
+of numba's float64).
+
+Look-back scratch is cached per (device, stream) and reused with epoch tags,
+so steady-state calls allocate nothing and memset nothing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+
+# torch / numpy dtype -> C-ABI code
+_TORCH_CODES = {
+    torch.int32: 1, torch.int64: 2, torch.uint32: 3, torch.uint64: 4, torch.float32: 5, torch.float64: 6,
+}
+_NP_CODES = {
+    np.dtype(np.int32): 1, np.dtype(np.int64): 2, np.dtype(np.uint32): 3, np.dtype(np.uint64): 4,
+    np.dtype(np.float32): 5, np.dtype(np.float64): 6,
+}
+_ACC_TORCH = {1: torch.int64, 2: torch.int64, 3: torch.uint64, 4: torch.uint64, 5: torch.float64, 6: torch.float64}
+_ELEM_BYTES = {1: 4, 2: 8, 3: 4, 4: 8, 5: 4, 6: 8}
+
+
+def dtype_code(dt) -> int:
+    if isinstance(dt, torch.dtype):
+        code = _TORCH_CODES.get(dt)
+    else:
+        code = _NP_CODES.get(np.dtype(dt))
+    if code is None:
+        raise ValueError(f"unsupported element dtype {dt}; expected one of int32, int64, uint32, "
+                         "uint64, float32, float64")
+    return code
+
+
+def acc_dtype(dt) -> torch.dtype:
+    return _ACC_TORCH[dtype_code(dt)]
+
+
+def acc_bits(value, code: int) -> int:
+    """Host scalar -> 8-byte accumulator bits (coerce_offset, core.py:40-48)."""
+    if code in (5, 6):
+        return struct.unpack("<Q", struct.pack("<d", float(value)))[0]
+    return int(value) & 0xFFFFFFFFFFFFFFFF
+
+
+def elem_bits(value, code: int) -> int:
+    """Host scalar -> element bits (wrap_element, core.py:51-55)."""
+    if code == 5:
+        return struct.unpack("<I", struct.pack("<f", float(value)))[0]
+    if code == 6:
+        return struct.unpack("<Q", struct.pack("<d", float(value)))[0]
+    if code in (1, 3):
+        return int(value) & 0xFFFFFFFF
+    return int(value) & 0xFFFFFFFFFFFFFFFF
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+
+
+class _Scratch:
+    """Zero-initialised, epoch-tagged look-back scratch for one (device, stream)."""
+
+    def __init__(self):
+        self.buf: torch.Tensor | None = None
+        self.epoch = 0
+
+    def take(self, nbytes: int, n_epochs: int, device: torch.device) -> tuple[int, int, int]:
+        if self.buf is None or self.buf.numel() < nbytes:
+            size = max(nbytes, 1 << 16)
+            if self.buf is not None:
+                size = max(size, 2 * self.buf.numel())
+            self.buf = torch.zeros(size, dtype=torch.uint8, device=device)
+            self.epoch = 0
+        if self.epoch + n_epochs > _lib.PS_EPOCH_MAX:
+            self.buf.zero_()
+            self.epoch = 0
+        first = self.epoch + 1
+        self.epoch += n_epochs
+        return self.buf.data_ptr(), self.buf.numel(), first
+
+
+_scratch: dict[tuple[int, int], _Scratch] = {}
+_scratch_lock = threading.Lock()
+
+
+def _scratch_for(device: torch.device, nbytes: int, n_epochs: int = 1):
+    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream_ptr(device))
+    with _scratch_lock:
+        s = _scratch.get(key)
+        if s is None:
+            s = _scratch[key] = _Scratch()
+        return s.take(nbytes, n_epochs, device)
+
+
+def _flat(t: torch.Tensor, name: str) -> torch.Tensor:
+    if t.dim() != 1:
+        raise ValueError(f"{name} must be 1-D, got shape {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def scan(x: torch.Tensor, out: torch.Tensor | None = None, *, exclusive: bool = False, seed=0,
+         seed_terms: torch.Tensor | None = None, total: torch.Tensor | None = None) -> torch.Tensor:
+    """out[i] = seed + sum(seed_terms) + sum(x[:i+1]) (exclusive: x[:i]).
+
+    ``out`` defaults to ``x`` (in place).  Returns the 1-element device total
+    (seed + sum(x)) in the accumulator dtype; nothing is synchronised."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    out = x if out is None else out
+    _require_cuda(out, "out")
+    _flat(out, "out")
+    if out.shape != x.shape:
+        raise ValueError("output buffer must match input shape")
+    ci, co = dtype_code(x.dtype), dtype_code(out.dtype)
+    lib = _lib.load()
+    if not lib.ps_pair_supported(ci, co):
+        raise ValueError(f"unsupported dtype pair {x.dtype} -> {out.dtype}")
+    if total is None:
+        total = torch.empty(1, dtype=_ACC_TORCH[ci], device=x.device)
+    n_terms = 0
+    if seed_terms is not None:
+        _require_cuda(seed_terms, "seed_terms")
+        if seed_terms.dtype != _ACC_TORCH[ci] or not seed_terms.is_contiguous():
+            raise ValueError(f"seed_terms must be contiguous {_ACC_TORCH[ci]}")
+        n_terms = seed_terms.numel()
+    n = x.numel()
+    sptr, sbytes, epoch = _scratch_for(x.device, lib.ps_scan_scratch_bytes(n, ci, co))
+    rc = lib.ps_scan(_ptr(x), _ptr(out), n, ci, co, int(bool(exclusive)), acc_bits(seed, ci),
+                     _ptr(seed_terms), n_terms, _ptr(total), sptr, sbytes, epoch, _stream_ptr(x.device))
+    _lib.check(rc, "ps_scan")
+    return total
+
+
+def reduce(x: torch.Tensor, *, seed=0, seed_terms: torch.Tensor | None = None,
+           total: torch.Tensor | None = None) -> torch.Tensor:
+    """Read-only total: seed + sum(seed_terms) + sum(x) as a 1-element device tensor."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    ci = dtype_code(x.dtype)
+    lib = _lib.load()
+    if total is None:
+        total = torch.empty(1, dtype=_ACC_TORCH[ci], device=x.device)
+    n_terms = 0 if seed_terms is None else seed_terms.numel()
+    sptr, sbytes, _ = _scratch_for(x.device, lib.ps_reduce_scratch_bytes(x.numel(), ci), 0)
+    rc = lib.ps_reduce(_ptr(x), x.numel(), ci, acc_bits(seed, ci), _ptr(seed_terms), n_terms, _ptr(total),
+                       sptr, sbytes, _stream_ptr(x.device))
+    _lib.check(rc, "ps_reduce")
+    return total
+
+
+def add_offset(x: torch.Tensor, delta=0, delta_terms: torch.Tensor | None = None) -> None:
+    """x += delta + sum(delta_terms), in the accumulator dtype."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    ci = dtype_code(x.dtype)
+    n_terms = 0 if delta_terms is None else delta_terms.numel()
+    rc = _lib.load().ps_add_offset(_ptr(x), x.numel(), ci, acc_bits(delta, ci), _ptr(delta_terms), n_terms,
+                                   _stream_ptr(x.device))
+    _lib.check(rc, "ps_add_offset")
+
+
+def shift_right(x: torch.Tensor, out: torch.Tensor | None = None, identity=0,
+                last: torch.Tensor | None = None) -> torch.Tensor | None:
+    """out[0] = identity, out[i] = x[i-1]; returns the displaced x[-1] as a
+    1-element device tensor (element dtype), or None when x is empty."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    out = x if out is None else out
+    if out.shape != x.shape or out.dtype != x.dtype:
+        raise ValueError("output buffer must match input shape and dtype")
+    ci = dtype_code(x.dtype)
+    n = x.numel()
+    if n == 0:
+        return None
+    if last is None:
+        last = torch.empty(1, dtype=x.dtype, device=x.device)
+    lib = _lib.load()
+    sptr, sbytes, _ = _scratch_for(x.device, lib.ps_shift_right_scratch_bytes(n, ci), 0)
+    rc = lib.ps_shift_right(_ptr(x), _ptr(out), n, ci, elem_bits(identity, ci), _ptr(last), sptr, sbytes,
+                            _stream_ptr(x.device))
+    _lib.check(rc, "ps_shift_right")
+    return last
+
+
+def _rows_view(x: torch.Tensor, name: str) -> tuple[int, int, int]:
+    if x.dim() != 2:
+        raise ValueError(f"{name} must be 2-D (rows, cols)")
+    if x.stride(1) != 1 and x.shape[1] > 1:
+        raise ValueError(f"{name} rows must be contiguous")
+    rows, cols = x.shape
+    ld = x.stride(0) if rows > 1 else cols
+    return rows, cols, ld
+
+
+def scan_batched(x: torch.Tensor, out: torch.Tensor | None = None, *, exclusive: bool = False,
+                 row_seeds: torch.Tensor | None = None, row_totals: torch.Tensor | None = None) -> None:
+    """Independent scans of every row of a 2-D tensor (row-major, any row stride)."""
+    _require_cuda(x, "x")
+    out = x if out is None else out
+    _require_cuda(out, "out")
+    rows, cols, ld_in = _rows_view(x, "x")
+    r2, c2, ld_out = _rows_view(out, "out")
+    if (r2, c2) != (rows, cols):
+        raise ValueError("output buffer must match input shape")
+    ci, co = dtype_code(x.dtype), dtype_code(out.dtype)
+    lib = _lib.load()
+    if not lib.ps_pair_supported(ci, co):
+        raise ValueError(f"unsupported dtype pair {x.dtype} -> {out.dtype}")
+    for t, nm in ((row_seeds, "row_seeds"), (row_totals, "row_totals")):
+        if t is not None and (t.dtype != _ACC_TORCH[ci] or t.numel() != rows or not t.is_contiguous()):
+            raise ValueError(f"{nm} must be a contiguous {_ACC_TORCH[ci]} tensor of {rows} entries")
+    sptr, sbytes, epoch = _scratch_for(x.device, lib.ps_scan_batched_scratch_bytes(rows, cols, ci, co))
+    rc = lib.ps_scan_batched(_ptr(x), _ptr(out), rows, cols, ld_in, ld_out, ci, co, int(bool(exclusive)),
+                             _ptr(row_seeds), _ptr(row_totals), sptr, sbytes, epoch, _stream_ptr(x.device))
+    _lib.check(rc, "ps_scan_batched")
+
+
+def reduce_batched(x: torch.Tensor, row_totals: torch.Tensor | None = None) -> torch.Tensor:
+    _require_cuda(x, "x")
+    rows, cols, ld = _rows_view(x, "x")
+    ci = dtype_code(x.dtype)
+    if row_totals is None:
+        row_totals = torch.empty(rows, dtype=_ACC_TORCH[ci], device=x.device)
+    rc = _lib.load().ps_reduce_batched(_ptr(x), rows, cols, ld, ci, _ptr(row_totals), _stream_ptr(x.device))
+    _lib.check(rc, "ps_reduce_batched")
+    return row_totals
+
+
+def add_offset_batched(x: torch.Tensor, row_deltas: torch.Tensor) -> None:
+    _require_cuda(x, "x")
+    rows, cols, ld = _rows_view(x, "x")
+    ci = dtype_code(x.dtype)
+    if row_deltas.dtype != _ACC_TORCH[ci] or row_deltas.numel() != rows:
+        raise ValueError(f"row_deltas must be {_ACC_TORCH[ci]} with {rows} entries")
+    rc = _lib.load().ps_add_offset_batched(_ptr(x), rows, cols, ld, ci, _ptr(row_deltas), _stream_ptr(x.device))
+    _lib.check(rc, "ps_add_offset_batched")
+
+
+def scan_segmented(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None, *,
+                   exclusive: bool = False, seg_totals: torch.Tensor | None = None) -> torch.Tensor | None:
+    """Scan every CSR segment x[offsets[s]:offsets[s+1]] independently."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    out = x if out is None else out
+    _flat(out, "out")
+    if offsets.dtype != torch.int64 or offsets.dim() != 1 or not offsets.is_cuda or not offsets.is_contiguous():
+        raise ValueError("offsets must be a contiguous 1-D int64 CUDA tensor")
+    nseg = offsets.numel() - 1
+    if nseg < 0:
+        raise ValueError("offsets needs at least one entry")
+    ci, co = dtype_code(x.dtype), dtype_code(out.dtype)
+    lib = _lib.load()
+    if seg_totals is not None and (seg_totals.dtype != _ACC_TORCH[ci] or seg_totals.numel() != nseg):
+        raise ValueError(f"seg_totals must be {_ACC_TORCH[ci]} with {nseg} entries")
+    sptr, sbytes, epoch = _scratch_for(x.device, lib.ps_scan_segmented_scratch_bytes(x.numel(), ci, co))
+    rc = lib.ps_scan_segmented(_ptr(x), _ptr(out), x.numel(), _ptr(offsets), nseg, ci, co, int(bool(exclusive)),
+                               _ptr(seg_totals), sptr, sbytes, epoch, _stream_ptr(x.device))
+    _lib.check(rc, "ps_scan_segmented")
+    return seg_totals
+
+
+def wrapped_block_total(x: torch.Tensor, w: int, seed=0) -> torch.Tensor:
+    """uint32 total with every w-block summed mod 2^32 (simd.py:84-99)."""
+    _require_cuda(x, "x")
+    if x.dtype != torch.uint32:
+        raise ValueError("wrapped block totals are defined for uint32 data only")
+    total = torch.empty(1, dtype=torch.uint64, device=x.device)
+    rc = _lib.load().ps_reduce_wrapped_blocks(_ptr(x), x.numel(), w, acc_bits(seed, 3), _ptr(total),
+                                              _stream_ptr(x.device))
+    _lib.check(rc, "ps_reduce_wrapped_blocks")
+    return total
+
+
+# ---- host buffers: the end-to-end entry point ---------------------------------------------------
+DEFAULT_CHUNK_BYTES = 64 << 20
+
+
+class _HostWorkspace:
+    def __init__(self):
+        self.buf = None
+        self.epoch = 0
+
+
+_host_ws: dict[int, _HostWorkspace] = {}
+
+
+def _host_pointer(a) -> tuple[int, int, int]:
+    """(address, numel, dtype code) of a host numpy array or CPU tensor."""
+    if isinstance(a, np.ndarray):
+        if a.ndim != 1 or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("host buffers must be contiguous 1-D arrays")
+        return a.ctypes.data, a.shape[0], dtype_code(a.dtype)
+    if isinstance(a, torch.Tensor) and not a.is_cuda:
+        if a.dim() != 1 or not a.is_contiguous():
+            raise ValueError("host buffers must be contiguous 1-D tensors")
+        return a.data_ptr(), a.numel(), dtype_code(a.dtype)
+    raise ValueError("expected a host numpy array or CPU tensor")
+
+
+def scan_host(x, out=None, *, exclusive: bool = False, seed=0, chunk_elems: int | None = None,
+              device: torch.device | int | None = None):
+    """Scan HOST memory end to end (H2D -> look-back scan -> D2H, pipelined in
+    chunks over three streams).  ``out`` defaults to ``x`` (in place).  Pinned
+    host memory gives full PCIe overlap; pageable memory works but serialises.
+    Blocks; returns the accumulator-precision total as a Python number."""
+    xp, n, ci = _host_pointer(x)
+    out = x if out is None else out
+    op, n2, co = _host_pointer(out)
+    if n2 != n:
+        raise ValueError("output buffer must match input shape")
+    lib = _lib.load()
+    if not lib.ps_pair_supported(ci, co):
+        raise ValueError("unsupported dtype pair")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       (device if isinstance(device, int) else device.index or 0))
+    if chunk_elems is None:
+        chunk_elems = max(DEFAULT_CHUNK_BYTES // max(_ELEM_BYTES[ci], _ELEM_BYTES[co]), 1 << 16)
+    wsb = lib.ps_scan_host_workspace_bytes(chunk_elems, ci, co)
+    nep = lib.ps_scan_host_epochs(n, chunk_elems)
+    with torch.cuda.device(dev):
+        ws = _host_ws.setdefault(dev.index, _HostWorkspace())
+        if ws.buf is None or ws.buf.numel() < wsb:
+            ws.buf = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+            ws.epoch = 0
+        if ws.epoch + nep > _lib.PS_EPOCH_MAX:
+            ws.buf.zero_()
+            ws.epoch = 0
+        epoch = ws.epoch + 1
+        ws.epoch += nep
+        tot = np.zeros(1, np.uint64)
+        rc = lib.ps_scan_host(xp, op, n, ci, co, int(bool(exclusive)), acc_bits(seed, ci), tot.ctypes.data,
+                              ws.buf.data_ptr(), ws.buf.numel(), chunk_elems, epoch, _stream_ptr(dev))
+        _lib.check(rc, "ps_scan_host")
+    return acc_to_python(tot.view(np.dtype(_acc_np(ci)))[0], ci)
+
+
+def _acc_np(code: int):
+    return np.float64 if code in (5, 6) else (np.uint64 if code in (3, 4) else np.int64)
+
+
+def acc_to_python(v, code: int):
+    if code in (5, 6):
+        return float(v)
+    return int(v)
+
+
+def total_to_python(t: torch.Tensor, code: int):
+    """1-element device accumulator -> Python scalar (synchronises)."""
+    v = t.cpu()
+    if v.dtype == torch.uint64:
+        return int(v.view(torch.int64).item()) & 0xFFFFFFFFFFFFFFFF
+    return acc_to_python(v.item(), code)

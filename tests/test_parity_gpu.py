@@ -1,0 +1,460 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's own
+outputs (golden vectors), the C oracle, and numpy, on the reference's entry
+points and on BASELINE.json's configs.
+
+Tolerances: integer dtypes are compared bit-exactly.  float32 outputs must be
+within rtol 1e-6 of the reference (its own harness allows 1e-5,
+bench.py:24; BASELINE.json allows 1e-4): the GPU carries float64 like the
+reference but reassociates.  On the config generators (multiples of 2^-24,
+partial sums < 2^29) float64 partial sums are exact, so cfg2 is asserted
+bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_cases as G
+from conftest import assert_scan_matches, make_data
+
+pytestmark = pytest.mark.gpu
+
+FLOAT_RTOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def ps():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2312_14874_b200 as ps
+    from paper_2312_14874_b200 import _lib
+    _lib.load()
+    return ps
+
+
+def _cuda(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def _beyond_2_53(case, inp):
+    return inp.dtype.kind == "i" and inp.size and np.abs(inp.astype(np.float64)).sum() >= 2.0**53
+
+
+def _assert_total(got, case):
+    want = G.total_of(case)
+    if want is None:
+        return
+    if isinstance(want, float) and case["dtype"] in ("float32", "float64"):
+        assert got == pytest.approx(want, rel=1e-12, abs=1e-12), (got, want)
+    else:
+        assert int(got) == int(want), (got, want)
+
+
+def _assert_array(got, want, ctx):
+    if want.dtype.kind == "f":
+        assert_scan_matches(got, want, rtol=FLOAT_RTOL, context=ctx)
+    else:
+        assert np.array_equal(got, want), ctx
+
+
+SCAN_CASES = [c for c, _, _ in G.cases() if c["op"] in (
+    "sequential_inclusive_scan", "horizontal_scan", "vertical_scan", "tree_scan", "tree_scan_auto",
+    "sequential_accumulate", "sequential_increment", "exclusive_from_inclusive", "engine")]
+
+
+@pytest.mark.parametrize("case", SCAN_CASES, ids=[G.case_id(c) for c in SCAN_CASES])
+@pytest.mark.parametrize("where", ["cuda", "numpy"])
+def test_golden_through_dropin(ps, case, where):
+    _, arrays = G.load()
+    inp, want = arrays[case["in"]], arrays[case["out"]]
+    if _beyond_2_53(case, inp):
+        pytest.skip("reference float64 accumulator is lossy here; see test_int64_beyond_2_53_is_exact")
+    data = _cuda(inp) if where == "cuda" else inp.copy()
+    op = case["op"]
+    total = None
+    out = None
+    if op == "sequential_inclusive_scan":
+        total = ps.sequential_inclusive_scan(data, ps.Span(case["start"], case["len"]), case["offset"])
+    elif op == "horizontal_scan":
+        if case["out_of_place"]:
+            out = torch.zeros_like(data) if where == "cuda" else np.zeros_like(inp)
+        total = ps.horizontal_scan(data, ps.Span(case["start"], case["len"]), case["offset"], case["w"], out=out)
+    elif op == "vertical_scan":
+        total = ps.vertical_scan(data, ps.Span(case["start"], case["len"]), case["offset"], case["w"],
+                                 case["scan_in_pass1"], case["block_len"])
+    elif op == "tree_scan":
+        total = ps.tree_scan(data, ps.Span(case["start"], case["len"]), case["offset"], case["w"])
+    elif op == "tree_scan_auto":
+        total = ps.tree_scan_auto(data, ps.Span(case["start"], case["len"]), case["offset"], case["w"],
+                                  case["block_len"])
+    elif op == "sequential_accumulate":
+        total = ps.sequential_accumulate(data, ps.Span(case["start"], case["len"]))
+    elif op == "sequential_increment":
+        ps.sequential_increment(data, ps.Span(case["start"], case["len"]), case["offset"])
+    elif op == "exclusive_from_inclusive":
+        total = ps.exclusive_from_inclusive(data, case["identity"])
+    elif op == "engine":
+        out = torch.empty_like(data) if where == "cuda" else np.empty_like(inp)
+        req = ps.ScanRequest(data=data, out=out, kernel=case["kernel"], scheme=ps.SchemeId(case["scheme"]),
+                             block_len=case["block_len"], threads=case["threads"])
+        total = ps.execute(req)
+    res = out if out is not None else data
+    got = _host(res) if where == "cuda" else res
+    _assert_array(got, want, G.case_id(case))
+    if op == "sequential_accumulate" or op == "sequential_increment":
+        assert np.array_equal(_host(data) if where == "cuda" else data, want)  # read-only / in place
+    if total is not None:
+        _assert_total(total, case)
+
+
+def test_int64_beyond_2_53_is_exact(ps):
+    """Divergence pin: above 2^53 the reference's float64 accumulator rounds;
+    the GPU keeps exact int64 (two's complement) arithmetic."""
+    x = np.array([1, 2, 3, 2**60, 2**62], np.int64)
+    t = _cuda(x)
+    total = ps.sequential_inclusive_scan(t, ps.full_span(t))
+    assert np.array_equal(_host(t), np.cumsum(x))
+    assert total == int(np.sum(x))
+
+
+def test_widen_exclusive_golden(ps):
+    from paper_2312_14874_b200 import device
+    (case, inp, want), = list(G.cases("widen_exclusive"))
+    x = _cuda(inp)
+    out = torch.empty(inp.shape[0], dtype=torch.int64, device="cuda")
+    total = device.scan(x, out, exclusive=True)
+    assert np.array_equal(_host(out), want)
+    assert int(total.item()) == G.total_of(case) == int(inp.sum())
+
+
+def test_rows_widen_golden(ps):
+    from paper_2312_14874_b200 import device
+    (case, inp, want), = list(G.cases("rows_widen_inclusive"))
+    x = _cuda(inp)
+    out = torch.empty(inp.shape, dtype=torch.int64, device="cuda")
+    tot = torch.empty(inp.shape[0], dtype=torch.int64, device="cuda")
+    device.scan_batched(x, out, row_totals=tot)
+    assert np.array_equal(_host(out), want)
+    assert np.array_equal(_host(tot), want[:, -1])
+
+
+# ---- edge cases: sizes around tile boundaries, alignment, in/out of place ----------------------
+
+TILE = {np.int64: 4096, np.int32: 8192, np.uint32: 8192, np.float32: 8192, np.float64: 4096, np.uint64: 4096}
+GENS = {
+    np.int64: lambda r, n: r.integers(-1000, 1001, n, dtype=np.int64),
+    np.int32: lambda r, n: r.integers(-(2**31), 2**31, n, dtype=np.int32),
+    np.uint32: lambda r, n: r.integers(0, 2**32, n, dtype=np.uint32),
+    np.uint64: lambda r, n: r.integers(0, 2**63, n, dtype=np.uint64),
+    np.float32: lambda r, n: r.random(n, dtype=np.float32),
+    np.float64: lambda r, n: r.random(n),
+}
+
+
+def _expected(x, seed=0, exclusive=False, out_dtype=None):
+    out_dtype = out_dtype or x.dtype
+    if x.dtype.kind == "f":
+        inc = np.cumsum(x.astype(np.float64)) + float(seed)
+    elif x.dtype == np.uint32 or x.dtype == np.uint64:
+        inc = np.cumsum(x.astype(np.uint64)) + np.uint64(seed)
+    else:
+        inc = np.cumsum(x.astype(np.int64)) + np.int64(seed)
+    if exclusive:
+        inc = np.concatenate([np.array([seed], inc.dtype), inc[:-1]]) if len(inc) else inc
+    return inc.astype(out_dtype)
+
+
+@pytest.mark.parametrize("dt", list(GENS))
+def test_sizes_around_tiles(ps, dt):
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(11)
+    T = TILE[dt]
+    for n in (0, 1, 2, 31, 32, 33, T - 1, T, T + 1, 2 * T - 1, 33 * T + 5, 70 * T + 3):
+        x = GENS[dt](r, n)
+        for exclusive in (False, True):
+            t = _cuda(x)
+            out = torch.empty_like(t)
+            seed = 7 if dt != np.float32 else 0.5
+            total = device.scan(t, out, exclusive=exclusive, seed=seed)
+            ctx = f"{dt.__name__} n={n} excl={exclusive}"
+            _assert_array(_host(out), _expected(x, seed, exclusive), ctx)
+            tv = total.cpu().numpy()[0]
+            exp_total = (_expected(x, seed, False, np.float64 if x.dtype.kind == "f" else None)[-1]
+                         if n else seed)
+            if x.dtype.kind == "f":
+                assert abs(float(tv) - float(exp_total)) <= 1e-9 * max(1.0, abs(float(exp_total))), ctx
+            elif dt in (np.uint32, np.uint64):
+                assert int(tv) == (int(x.astype(np.uint64).sum(dtype=np.uint64)) + 7) % 2**64, ctx
+            else:
+                assert int(tv) == int(x.astype(np.int64).sum()) + 7, ctx
+
+
+@pytest.mark.parametrize("dt", [np.int64, np.float32, np.uint32, np.int32])
+def test_unaligned_starts(ps, dt):
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(3)
+    T = TILE[dt]
+    base = GENS[dt](r, 5 * T + 100)
+    for s_in in range(0, 9):
+        for s_out in (s_in, (s_in + 1) % 9, 0):
+            n = 3 * T + 17
+            x = _cuda(base)
+            o = torch.zeros(base.shape[0] + 16, dtype=x.dtype, device="cuda")
+            xin, xout = x[s_in:s_in + n], o[s_out:s_out + n]
+            device.scan(xin, xout)
+            _assert_array(_host(xout), _expected(base[s_in:s_in + n]), f"{dt.__name__} in@{s_in} out@{s_out}")
+            assert np.array_equal(_host(x), base)  # out of place leaves the input alone
+            # in place on the unaligned view
+            device.scan(xin)
+            _assert_array(_host(x)[s_in:s_in + n], _expected(base[s_in:s_in + n]), f"inplace@{s_in}")
+            assert np.array_equal(_host(x)[:s_in], base[:s_in])
+            assert np.array_equal(_host(x)[s_in + n:], base[s_in + n:])
+
+
+def test_seed_terms_and_total_chaining(ps):
+    """Chunked scans seeded with the previous chunk's device total equal one scan
+    (the pattern the multi-GPU carry and the host pipeline rely on)."""
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(5)
+    x = r.integers(0, 1001, 1_000_003, dtype=np.int64)
+    t = _cuda(x)
+    carry = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bounds = [0, 1, 4096, 5000, 123_457, 999_999, 1_000_003]
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        device.scan(t[a:b], seed_terms=carry.clone(), total=carry)
+    assert np.array_equal(_host(t), np.cumsum(x))
+    terms = torch.tensor([5, -3, 11], dtype=torch.int64, device="cuda")
+    y = _cuda(x[:10000])
+    tot = device.scan(y, seed=100, seed_terms=terms)
+    assert np.array_equal(_host(y), np.cumsum(x[:10000]) + 113)
+    assert int(tot.item()) == int(x[:10000].sum()) + 113
+
+
+def test_float32_double_accumulation_matches_reference_bitwise(ps):
+    """uniform [0,1) float32 (multiples of 2^-24): every float64 partial sum is
+    exact, so the GPU equals float32(cumsum(float64)) -- the reference -- bit for bit."""
+    from paper_2312_14874_b200 import device
+    x = np.random.default_rng(1).random(1 << 22, dtype=np.float32)
+    t = _cuda(x)
+    device.scan(t)
+    assert np.array_equal(_host(t), np.cumsum(x.astype(np.float64)).astype(np.float32))
+
+
+def test_batched_rows_edge_cases(ps):
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(8)
+    for rows, cols, ld in ((1, 1, 1), (3, 5, 8), (7, 8192, 8192), (5, 8193, 8200), (64, 100_000, 100_000),
+                           (2, 0, 4)):
+        x = r.integers(0, 256, (rows, ld), dtype=np.int32)
+        xt = _cuda(x)[:, :cols]
+        out = torch.empty((rows, cols), dtype=torch.int64, device="cuda")
+        seeds = torch.arange(rows, dtype=torch.int64, device="cuda") * 1000
+        tots = torch.empty(rows, dtype=torch.int64, device="cuda")
+        for excl in (False, True):
+            device.scan_batched(xt, out, exclusive=excl, row_seeds=seeds, row_totals=tots)
+            inc = np.cumsum(x[:, :cols].astype(np.int64), axis=1) + (np.arange(rows) * 1000)[:, None]
+            exp = inc if not excl else np.concatenate([(np.arange(rows) * 1000)[:, None], inc[:, :-1]], axis=1)
+            if cols:
+                assert np.array_equal(_host(out), exp), (rows, cols, excl)
+            assert np.array_equal(_host(tots), inc[:, -1] if cols else np.arange(rows) * 1000)
+
+
+def test_segmented(ps):
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(9)
+    for n, nseg in ((0, 1), (1, 1), (10, 3), (50_000, 1), (100_000, 7), (300_001, 1000), (40_000, 40_000)):
+        x = r.integers(0, 100, n, dtype=np.int32)
+        cuts = np.sort(r.integers(0, n + 1, nseg - 1)) if nseg > 1 else np.array([], np.int64)
+        offs = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+        for excl in (False, True):
+            xt = _cuda(x)
+            out = torch.empty(n, dtype=torch.int64, device="cuda")
+            tots = torch.empty(nseg, dtype=torch.int64, device="cuda")
+            device.scan_segmented(xt, _cuda(offs), out, exclusive=excl, seg_totals=tots)
+            exp = np.empty(n, np.int64)
+            exp_tot = np.zeros(nseg, np.int64)
+            for s in range(nseg):
+                seg = x[offs[s]:offs[s + 1]].astype(np.int64)
+                c = np.cumsum(seg)
+                exp[offs[s]:offs[s + 1]] = c - seg if excl else c
+                exp_tot[s] = seg.sum()
+            assert np.array_equal(_host(out), exp), (n, nseg, excl)
+            assert np.array_equal(_host(tots), exp_tot), (n, nseg)
+
+
+def test_shift_right_in_place_large(ps):
+    from paper_2312_14874_b200 import device
+    x = np.random.default_rng(2).integers(0, 2**40, 1_000_001, dtype=np.int64)
+    t = _cuda(x)
+    last = device.shift_right(t, identity=-5)
+    assert int(last.item()) == int(x[-1])
+    assert np.array_equal(_host(t), np.concatenate([[-5], x[:-1]]))
+
+
+def test_reduce_and_add_offset_large(ps):
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(4)
+    for dt in (np.int64, np.float32, np.uint32, np.int32):
+        x = GENS[dt](r, 3_000_017)
+        for s in (0, 1, 3):
+            t = _cuda(x)[s:]
+            tot = device.reduce(t, seed=2)
+            if x.dtype.kind == "f":
+                assert abs(tot.item() - (x[s:].astype(np.float64).sum() + 2)) < 1e-6 * x.size
+            elif dt == np.uint32:
+                assert int(tot.cpu().view(torch.int64).item()) == int(x[s:].astype(np.uint64).sum()) + 2
+            else:
+                assert int(tot.item()) == int(x[s:].astype(np.int64).sum()) + 2
+            device.add_offset(t, 3)
+            exp = (x[s:].astype(np.float64) + 3).astype(dt) if x.dtype.kind == "f" else (x[s:] + dt(3)).astype(dt)
+            assert np.array_equal(_host(t), exp), dt
+
+
+def test_reduce_is_deterministic(ps):
+    from paper_2312_14874_b200 import device
+    x = _cuda(np.random.default_rng(6).standard_normal(10_000_019).astype(np.float32))
+    vals = {device.reduce(x).item() for _ in range(5)}
+    assert len(vals) == 1
+
+
+def test_host_pipeline_end_to_end(ps):
+    """ps_scan_host: pinned and pageable host buffers, chunk boundaries, seeds."""
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(12)
+    x = r.integers(0, 101, 3_000_001, dtype=np.int64)
+    for chunk in (1 << 16, 1_000_000, 1 << 22):
+        pinned_in = torch.from_numpy(x).pin_memory()
+        pinned_out = torch.empty_like(pinned_in).pin_memory()
+        tot = device.scan_host(pinned_in, pinned_out, seed=5, chunk_elems=chunk)
+        assert np.array_equal(pinned_out.numpy(), np.cumsum(x) + 5)
+        assert tot == int(x.sum()) + 5
+        y = x.copy()
+        tot = device.scan_host(y, exclusive=True, chunk_elems=chunk)  # pageable, in place
+        assert np.array_equal(y, np.concatenate([[0], np.cumsum(x)[:-1]]))
+        assert tot == int(x.sum())
+    f = r.random(2_000_003, dtype=np.float32)
+    g = np.empty(f.shape[0], np.float64)
+    device.scan_host(f, g, chunk_elems=1 << 18)
+    assert np.array_equal(g, np.cumsum(f.astype(np.float64)))
+
+
+def test_errors_match_reference(ps):
+    t = torch.zeros(4, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        ps.sequential_inclusive_scan(t, ps.Span(2, 3))
+    with pytest.raises(ValueError):
+        ps.horizontal_scan(t, ps.full_span(t), 0, w=5)
+    with pytest.raises(ValueError):
+        ps.tree_scan(torch.zeros(48, dtype=torch.uint32, device="cuda"), ps.Span(0, 48), 0, 16)
+    with pytest.raises(ValueError):
+        ps.ScanRequest(data=t, out=t)
+    with pytest.raises(ValueError):
+        ps.sequential_inclusive_scan(torch.zeros(4, dtype=torch.int16, device="cuda"), ps.Span(0, 4))
+
+
+def test_vertical_pass_functions(ps):
+    """The reference's step-level KATs (test_simd.py:109-183) against the GPU batched kernels."""
+    from paper_2312_14874_b200.simd import (exclusive_offsets, vertical_scan_pass1_accumulate,
+                                            vertical_scan_pass1_scan, vertical_scan_pass2_increment,
+                                            vertical_scan_pass2_scan)
+    for where in ("numpy", "cuda"):
+        data = np.array([1, 2, 3, 4, 5, 6, 7, 8], dtype=np.uint32)
+        d = _cuda(data) if where == "cuda" else data.copy()
+        totals = np.zeros(2, dtype=np.uint64)
+        vertical_scan_pass1_scan(d, ps.full_span(d), 0, totals)
+        assert (_host(d) if where == "cuda" else d).tolist() == [1, 3, 6, 10, 5, 11, 18, 26]
+        assert totals.tolist() == [10, 26]
+        vertical_scan_pass2_increment(d, ps.full_span(d), exclusive_offsets(totals, np.uint64(0)))
+        assert (_host(d) if where == "cuda" else d).tolist() == [1, 3, 6, 10, 15, 21, 28, 36]
+
+        d = _cuda(data) if where == "cuda" else data.copy()
+        vertical_scan_pass1_accumulate(d, ps.full_span(d), totals)
+        assert totals.tolist() == [10, 26]
+        vertical_scan_pass2_scan(d, ps.full_span(d), exclusive_offsets(totals, np.uint64(0)))
+        assert (_host(d) if where == "cuda" else d).tolist() == [1, 3, 6, 10, 15, 21, 28, 36]
+
+        d = np.array([3, 4, 5, 6], dtype=np.uint32)
+        totals = np.zeros(4, dtype=np.uint64)
+        dd = _cuda(d) if where == "cuda" else d
+        vertical_scan_pass1_scan(dd, ps.full_span(dd), 100, totals)
+        assert (_host(dd) if where == "cuda" else dd).tolist() == [103, 4, 5, 6]
+        assert totals.tolist() == [103, 4, 5, 6]
+
+
+# ---- BASELINE.json configs at full size ---------------------------------------------------------
+
+def test_cfg1_full(ps, oracle_lib):
+    x = np.random.default_rng(0).integers(0, 101, 2**24, dtype=np.int64)
+    want = x.copy()
+    wt = oracle_lib.scan(want, 0, want.shape[0], 0)  # the reference algorithm, restated
+    t = _cuda(x)
+    total = ps.sequential_inclusive_scan(t, ps.full_span(t))
+    assert np.array_equal(_host(t), want)
+    assert total == wt
+
+
+def test_cfg2_full(ps):
+    x = np.random.default_rng(1).random(2**28, dtype=np.float32)
+    ref = np.cumsum(x.astype(np.float64))
+    t = _cuda(x)
+    total = ps.sequential_inclusive_scan(t, ps.full_span(t))
+    got = _host(t)
+    assert np.array_equal(got, ref.astype(np.float32))  # exact partial sums -> bit-exact
+    rel = np.abs(got.astype(np.float64) - ref) / np.maximum(ref, 1e-30)
+    assert rel.max() <= 1e-4 and total == ref[-1]
+
+
+def test_cfg3_full(ps):
+    from paper_2312_14874_b200 import device
+    flags = np.random.default_rng(2).integers(0, 2, 2**28, dtype=np.int32)
+    t = _cuda(flags)
+    out = torch.empty(2**28, dtype=torch.int64, device="cuda")
+    total = device.scan(t, out, exclusive=True)
+    got = _host(out)
+    assert int(total.item()) == int(flags.sum())
+    assert got[0] == 0
+    assert np.array_equal(got[1:], np.cumsum(flags[:-1], dtype=np.int64))
+
+
+def test_cfg4_full(ps):
+    from paper_2312_14874_b200 import device
+    x = np.random.default_rng(3).integers(0, 256, (16384, 16384), dtype=np.int32)
+    t = _cuda(x)
+    out = torch.empty((16384, 16384), dtype=torch.int64, device="cuda")
+    device.scan_batched(t, out)
+    got = _host(out)
+    assert np.array_equal(got, np.cumsum(x, axis=1, dtype=np.int64))
+
+
+def test_cfg5_full_properties(ps):
+    """2^31 int64 (16 GB in + 16 GB out) on one GPU: generated on the device;
+    checked through size-independent properties -- first differences give the
+    input back, the total equals an independent reduction, and sampled windows
+    match numpy continued from the carry."""
+    from paper_2312_14874_b200 import device
+    n = 2**31
+    if torch.cuda.get_device_properties(0).total_memory < 40 * 2**30:
+        pytest.skip("needs > 40 GB of device memory")
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randint(0, 1001, (n,), dtype=torch.int64, device="cuda", generator=g)
+    out = torch.empty_like(x)
+    total = device.scan(x, out)
+    red = device.reduce(x)
+    assert int(total.item()) == int(red.item())
+    assert int(out[-1].item()) == int(total.item())
+    step = 1 << 28
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        d = out[a + 1:b] - out[a:b - 1]
+        assert torch.equal(d, x[a + 1:b])
+    assert int(out[0].item()) == int(x[0].item())
+    xs = x[:1 << 20].cpu().numpy()
+    assert np.array_equal(out[:1 << 20].cpu().numpy(), np.cumsum(xs))
+    for a in (n // 3, n - (1 << 20)):
+        w = x[a:a + (1 << 20)].cpu().numpy()
+        carry = int(out[a - 1].item())
+        assert np.array_equal(out[a:a + (1 << 20)].cpu().numpy(), np.cumsum(w) + carry)
