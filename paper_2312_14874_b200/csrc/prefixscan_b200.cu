@@ -49,18 +49,13 @@ int64_t tile_of_dtype(int dt) { return (int64_t)SCAN_WARPS * SCAN_ROWS * 32 * (i
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-size_t desc_bytes(int64_t tiles) {
-    return align_up((size_t)tiles * 4, 256) + 2 * align_up((size_t)tiles * 8, 256);
-}
+// look-back scratch: 256 bytes of control words, then one 16-byte descriptor per tile
+size_t desc_bytes(int64_t tiles) { return 256 + align_up((size_t)tiles * 16, 256); }
 
 Desc carve_desc(void *scratch, int64_t tiles) {
-    char *p = static_cast<char *>(scratch);
+    (void)tiles;
     Desc d;
-    d.flags = reinterpret_cast<uint32_t *>(p);
-    p += align_up((size_t)tiles * 4, 256);
-    d.agg = reinterpret_cast<uint64_t *>(p);
-    p += align_up((size_t)tiles * 8, 256);
-    d.incl = reinterpret_cast<uint64_t *>(p);
+    d.d = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
     return d;
 }
 

@@ -84,49 +84,64 @@ template <typename A> __device__ __forceinline__ A warp_sum(A v) {
     return v;
 }
 
-// Descriptor status values (low 2 bits of the epoch-tagged flag word).
-constexpr uint32_t ST_A = 1;  // aggregate published
-constexpr uint32_t ST_P = 2;  // inclusive prefix published
+// Descriptor status values (low 2 bits of the epoch-tagged status word).
+constexpr uint64_t ST_A = 1;  // aggregate published
+constexpr uint64_t ST_P = 2;  // inclusive prefix published
 
+// One 16-byte descriptor per tile: {(epoch << 2) | status, value bits}.  It is
+// written and read with single 128-bit strong accesses (st/ld.relaxed.gpu
+// .b128 -> STG/LDG.E.128.STRONG.GPU), so a reader sees status and value
+// together without fences: one L2 round trip per look-back window and no
+// acquire-induced L1 invalidation.
 struct Desc {
-    uint32_t *flags;  // (epoch << 2) | status, one per tile
-    uint64_t *agg;    // tile aggregate (acc bits)
-    uint64_t *incl;   // tile inclusive prefix (acc bits)
+    ulonglong2 *d;
 };
 
-__device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t epoch, uint32_t st,
-                                        uint64_t bits) {
-    st_relaxed_u64(st == ST_P ? d.incl + tile : d.agg + tile, bits);
-    st_release_u32(d.flags + tile, (epoch << 2) | st);
+__device__ __forceinline__ ulonglong2 ld_desc(const ulonglong2 *p) {
+    ulonglong2 v;
+    asm volatile("{ .reg .b128 t; ld.relaxed.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+                 : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_desc(ulonglong2 *p, uint64_t word, uint64_t value) {
+    asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.gpu.global.b128 [%0], t; }"
+                 ::"l"(p), "l"(word), "l"(value) : "memory");
+}
+
+__device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t epoch, uint64_t st, uint64_t bits) {
+    st_desc(d.d + tile, ((uint64_t)epoch << 2) | st, bits);
 }
 
 // Warp-parallel decoupled look-back (one full warp).  Returns the exclusive
 // prefix of `tile` within its segment [head, ...).  Lane j inspects tile
-// base-j; the window slides back 32 tiles until a P descriptor is seen.
-// Tiles before `head` are treated as P with value 0 (the head tile always
-// publishes P directly, so the scan never needs to read past it).
+// base-j; only the lanes in front of the nearest P descriptor have to be
+// valid, so older stragglers never stall a tile whose neighbour is done.
+// The window slides back 32 tiles when it holds no P.  Tiles before `head`
+// read as P with value 0 (the head tile publishes P itself).
 template <typename A>
 __device__ A lookback(const Desc &d, int64_t tile, int64_t head, uint32_t epoch, int lane) {
-    const uint32_t want = epoch << 2;
+    const uint64_t want = (uint64_t)epoch << 2;
     A excl = (A)0;
     int64_t base = tile - 1;
     while (true) {
         const int64_t p = base - lane;
         const bool live = p >= head;
-        uint32_t f = live ? ld_acquire_u32(d.flags + p) : (want | ST_P);
-        int spins = 0;
-        while (__any_sync(FULL, (f & ~3u) != want || (f & 3u) == 0)) {
-            if (++spins > 4) __nanosleep(spins > 64 ? 256 : 32);
-            if ((f & ~3u) != want || (f & 3u) == 0) f = ld_acquire_u32(d.flags + p);
+        ulonglong2 v = live ? ld_desc(d.d + p) : make_ulonglong2(want | ST_P, 0);
+        unsigned pmask, need;
+        int polls = 0;
+        while (true) {
+            const bool ok = (v.x & ~3ull) == want && (v.x & 3ull) != 0;
+            pmask = __ballot_sync(FULL, ok && (v.x & 3ull) == ST_P);
+            const unsigned xmask = __ballot_sync(FULL, !ok);
+            need = pmask ? ((pmask & (0u - pmask)) - 1) : FULL;  // lanes before the first P
+            if ((xmask & need) == 0) break;
+            if (++polls > 8) __nanosleep(polls > 64 ? 128 : 32);
+            if (!ok && ((need >> lane) & 1)) v = ld_desc(d.d + p);
         }
-        const unsigned pmask = __ballot_sync(FULL, (f & 3u) == ST_P);
         const int first_p = pmask ? __ffs(pmask) - 1 : 32;
-        A v = (A)0;
-        if (live) {
-            if (lane < first_p) v = acc_from_bits<A>(ld_relaxed_u64(d.agg + p));
-            else if (lane == first_p) v = acc_from_bits<A>(ld_relaxed_u64(d.incl + p));
-        }
-        excl += warp_sum(v);
+        A val = (A)0;
+        if (live && lane <= first_p) val = acc_from_bits<A>(v.y);
+        excl += warp_sum(val);
         if (pmask) return excl;
         base -= 32;
     }

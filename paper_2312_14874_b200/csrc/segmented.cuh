@@ -214,7 +214,7 @@ inline int64_t seg_tile_elems(int elem_bytes) { return (int64_t)8 * 4 * 32 * (32
 
 inline size_t seg_scratch_bytes(int64_t n, int elem_bytes) {
     const int64_t tiles = (n + seg_tile_elems(elem_bytes) - 1) / seg_tile_elems(elem_bytes) + 1;
-    return seg_align_up((size_t)tiles * 4, 256) + 2 * seg_align_up((size_t)tiles * 8, 256);
+    return 256 + seg_align_up((size_t)tiles * 16, 256);
 }
 
 template <typename TIn, typename TOut>
@@ -238,12 +238,7 @@ int launch_segmented(const void *in, void *out, int64_t n, const int64_t *offset
     a.lead = vec ? lead : 0;
     const int64_t tiles = (a.lead + n + TILE - 1) / TILE;
     if (tiles > 0x7fffffffLL) return 2;
-    char *p = static_cast<char *>(scratch);
-    a.desc.flags = reinterpret_cast<uint32_t *>(p);
-    p += seg_align_up((size_t)tiles * 4, 256);
-    a.desc.agg = reinterpret_cast<uint64_t *>(p);
-    p += seg_align_up((size_t)tiles * 8, 256);
-    a.desc.incl = reinterpret_cast<uint64_t *>(p);
+    a.desc.d = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
     seg_scan_kernel<TIn, TOut, 8, 4><<<(unsigned)tiles, 256, 0, s>>>(a);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : 1000 + (int)e;

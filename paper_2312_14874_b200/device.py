@@ -107,8 +107,8 @@ _scratch: dict[tuple[int, int], _Scratch] = {}
 _scratch_lock = threading.Lock()
 
 
-def _scratch_for(device: torch.device, nbytes: int, n_epochs: int = 1):
-    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream_ptr(device))
+def _scratch_for(device: torch.device, nbytes: int, n_epochs: int = 1, kind: str = "lookback"):
+    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream_ptr(device), kind)
     with _scratch_lock:
         s = _scratch.get(key)
         if s is None:
@@ -167,7 +167,7 @@ def reduce(x: torch.Tensor, *, seed=0, seed_terms: torch.Tensor | None = None,
     if total is None:
         total = torch.empty(1, dtype=_ACC_TORCH[ci], device=x.device)
     n_terms = 0 if seed_terms is None else seed_terms.numel()
-    sptr, sbytes, _ = _scratch_for(x.device, lib.ps_reduce_scratch_bytes(x.numel(), ci), 0)
+    sptr, sbytes, _ = _scratch_for(x.device, lib.ps_reduce_scratch_bytes(x.numel(), ci), 0, "reduce")
     rc = lib.ps_reduce(_ptr(x), x.numel(), ci, acc_bits(seed, ci), _ptr(seed_terms), n_terms, _ptr(total),
                        sptr, sbytes, _stream_ptr(x.device))
     _lib.check(rc, "ps_reduce")
@@ -201,7 +201,7 @@ def shift_right(x: torch.Tensor, out: torch.Tensor | None = None, identity=0,
     if last is None:
         last = torch.empty(1, dtype=x.dtype, device=x.device)
     lib = _lib.load()
-    sptr, sbytes, _ = _scratch_for(x.device, lib.ps_shift_right_scratch_bytes(n, ci), 0)
+    sptr, sbytes, _ = _scratch_for(x.device, lib.ps_shift_right_scratch_bytes(n, ci), 0, "shift")
     rc = lib.ps_shift_right(_ptr(x), _ptr(out), n, ci, elem_bits(identity, ci), _ptr(last), sptr, sbytes,
                             _stream_ptr(x.device))
     _lib.check(rc, "ps_shift_right")

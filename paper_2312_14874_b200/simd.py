@@ -288,7 +288,11 @@ def tree_scan_auto(data, span: Span, offset=0, w: int = DEFAULT_LANE_WIDTH, bloc
     idx = []
     for s0, ln, tree in pieces:
         idx.extend([s0 + ln - 1] if tree else range(s0, s0 + ln))
-    vals = res[idx].cpu().numpy() if is_device(res) else np.asarray(res)[idx]
+    if is_device(res):  # torch has no uint32 gather: index the int32 view, reinterpret on the host
+        sel = torch.tensor(idx, dtype=torch.int64, device=res.device)
+        vals = res.view(torch.int32)[sel].cpu().numpy().view(np.uint32)
+    else:
+        vals = np.asarray(res)[idx]
     acc = int(coerce_offset(offset, np.uint32))
     prev = acc & 0xFFFFFFFF
     for v in vals:  # each step is either a whole tree block or one tail element

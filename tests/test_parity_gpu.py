@@ -49,7 +49,10 @@ def _assert_total(got, case):
     if want is None:
         return
     if isinstance(want, float) and case["dtype"] in ("float32", "float64"):
-        assert got == pytest.approx(want, rel=1e-12, abs=1e-12), (got, want)
+        # the reference's horizontal / tree totals fold float32 block sums (simd.py:84-94,
+        # :330-334), so they sit ~1 float32 ulp from the float64 running total
+        rel = 1e-12 if case["op"] in ("sequential_inclusive_scan", "sequential_accumulate", "engine") else 1e-6
+        assert got == pytest.approx(want, rel=rel, abs=1e-12), (got, want)
     else:
         assert int(got) == int(want), (got, want)
 
