@@ -163,6 +163,16 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
                  int exclusive, uint64_t seed_bits, void *total_host, void *workspace,
                  size_t workspace_bytes, int64_t chunk_elems, uint32_t epoch, void *stream);
 
+/* Tuning knobs (process-wide; for benchmarks and tests):
+ *   "scan_kernel"      0 = auto, 1 = single-pass decoupled look-back,
+ *                      2 = cache-partitioned rounds (persistent, L2 regions)
+ *   "round_bytes"      input + output bytes per L2 region of the rounds kernel
+ *   "round_lead"       regions the rounds kernel's reducer warps run ahead
+ *   "rounds_min_bytes" auto mode uses the rounds kernel from this input size
+ * Returns PS_ERR_ARG for an unknown key or value. */
+int ps_set_tuning(const char *key, int64_t value);
+int64_t ps_get_tuning(const char *key); /* -1 for an unknown key */
+
 /* Human-readable text for a return code. */
 const char *ps_error_string(int code);
 

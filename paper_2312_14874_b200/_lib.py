@@ -42,6 +42,8 @@ SIGNATURES = {
     "ps_reduce_wrapped_blocks": (_i32, [_vp, _i64, _i32, _u64, _vp, _vp]),
     "ps_scan_host_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "ps_scan_host_epochs": (_i64, [_i64, _i64]),
+    "ps_set_tuning": (_i32, [ctypes.c_char_p, _i64]),
+    "ps_get_tuning": (_i64, [ctypes.c_char_p]),
     "ps_scan_host": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _u64, _vp, _vp, _sz, _i64, _u32, _vp]),
 }
 

@@ -13,6 +13,7 @@
 #include "scan_kernels.cuh"
 #include "segmented.cuh"
 #include "aux_kernels.cuh"
+#include "rounds_kernel.cuh"
 
 namespace ps {
 namespace {
@@ -69,6 +70,93 @@ bool overlaps_partially(const void *a, size_t abytes, const void *b, size_t bbyt
     return a0 < b1 && b0 < a1;
 }
 
+// ---- tuning (ps_set_tuning) ----------------------------------------------------------------
+struct Tuning {
+    int scan_kernel = 0;                    // 0 auto, 1 look-back, 2 cache-partitioned rounds
+    int64_t round_bytes = 48ll << 20;       // input + output bytes per L2 region (rounds kernel)
+    int64_t rounds_min_bytes = 16ll << 20;  // auto: rounds kernel from this many input bytes
+    int64_t round_lead = 2;                 // regions the reducer warps may run ahead of the scanners
+};
+Tuning g_tune;
+
+// rounds kernel: scanner warps, rows per warp, TMA stages, reducer warps, reducer lead (regions)
+constexpr int RW = 8, RR = 4, RS = 5, RRED = 4, RRS = 3;
+
+struct DevInfo {
+    int sms = 0;
+};
+DevInfo g_dev[64];
+
+int device_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!g_dev[dev].sms) cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    return g_dev[dev].sms;
+}
+
+template <typename TIn, typename TOut>
+int rounds_grid() {
+    using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
+    auto kern = scan_rounds_kernel<TIn, TOut, RW, RR, RS, RRED, RRS>;
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 0;
+    if (!per_sm[dev]) {
+        if (Geo::SMEM > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, Geo::THREADS, Geo::SMEM);
+        per_sm[dev] = b > 0 ? b : -1;
+    }
+    return per_sm[dev] > 0 ? per_sm[dev] * device_sms() : 0;
+}
+
+// geometry of the rounds kernel for n positions: (G, portion, rounds)
+template <typename TIn, typename TOut>
+bool rounds_plan(int64_t positions, int64_t &G, int64_t &portion, int64_t &rounds) {
+    using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
+    G = rounds_grid<TIn, TOut>();
+    if (G <= 0) return false;
+    int64_t want = g_tune.round_bytes / (int64_t)(sizeof(TIn) + sizeof(TOut)) / G;
+    portion = want / Geo::SUB * Geo::SUB;
+    if (portion < Geo::SUB) portion = Geo::SUB;
+    if (portion > (int64_t)Geo::MAX_CHUNKS * Geo::CHUNK) portion = (int64_t)Geo::MAX_CHUNKS * Geo::CHUNK / Geo::SUB * Geo::SUB;
+    rounds = (positions + portion * G - 1) / (portion * G);
+    return true;
+}
+
+template <typename TIn, typename TOut>
+int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclusive, uint64_t seed_bits,
+                  const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
+                  uint32_t epoch, cudaStream_t s) {
+    using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
+    int64_t G, portion, rounds;
+    if (!rounds_plan<TIn, TOut>(lead + n, G, portion, rounds)) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
+    if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
+    RoundArgs a{};
+    a.in = static_cast<const TIn *>(in) - lead;
+    a.out = static_cast<TOut *>(out) - lead;
+    a.lo = lead;
+    a.hi = lead + n;
+    a.round_elems = portion * G;
+    a.portion = portion;
+    a.rounds = rounds;
+    a.seed_bits = seed_bits;
+    a.seed_terms = seed_terms;
+    a.n_seed_terms = n_seed_terms;
+    a.total = total;
+    a.desc = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
+    a.epoch = epoch;
+    a.exclusive = exclusive;
+    a.lead_regions = (int)g_tune.round_lead;
+    void *params[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)scan_rounds_kernel<TIn, TOut, RW, RR, RS, RRED, RRS>,
+                                                dim3((unsigned)G), dim3(Geo::THREADS), params, Geo::SMEM, s);
+    return cuda_rc(e);
+}
+
 // ---- scan (1-D and batched share one kernel) ----------------------------------------------
 template <typename TIn, typename TOut>
 int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
@@ -98,6 +186,10 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     if (vec && lead * (int64_t)sizeof(TOut) >= 32) vec = false;
     a.vec_ok = vec;
     a.lead = vec ? lead : 0;
+    if (rows == 1 && vec && g_tune.scan_kernel != 1 &&
+        (g_tune.scan_kernel == 2 || cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes))
+        return launch_rounds<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
+                                        scratch, scratch_bytes, epoch, s);
     a.tiles_per_row = (a.lead + cols + TILE - 1) / TILE;
     const int64_t tiles = rows * a.tiles_per_row;
     if (tiles > 0x7fffffffLL) return PS_ERR_ARG;
@@ -244,7 +336,41 @@ const char *ps_error_string(int code) {
 size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     if (!pair_ok(dtype_in, dtype_out) || n < 0) return 0;
     const int64_t tile = tile_of_dtype(dtype_in);
-    return desc_bytes((n + tile - 1) / tile + 1);  // +1: a misaligned start can add a tile
+    size_t bytes = desc_bytes((n + tile - 1) / tile + 1);  // +1: a misaligned start can add a tile
+    // the cache-partitioned kernel needs one descriptor per (region, CTA); its
+    // grid is at most 8 CTAs per SM and regions are >= 1 MiB of input
+    const int64_t regions = (n * (int64_t)dsize(dtype_in)) / (1ll << 20) + 2;
+    const size_t rb = 256 + (size_t)regions * 8 * 160 * 16;
+    return bytes > rb ? bytes : rb;
+}
+
+int ps_set_tuning(const char *key, int64_t value) {
+    if (!key) return PS_ERR_ARG;
+    if (!std::strcmp(key, "scan_kernel")) {
+        if (value < 0 || value > 2) return PS_ERR_ARG;
+        g_tune.scan_kernel = (int)value;
+    } else if (!std::strcmp(key, "round_bytes")) {
+        if (value < (1ll << 20)) return PS_ERR_ARG;
+        g_tune.round_bytes = value;
+    } else if (!std::strcmp(key, "round_lead")) {
+        if (value < 1 || value > 8) return PS_ERR_ARG;
+        g_tune.round_lead = value;
+    } else if (!std::strcmp(key, "rounds_min_bytes")) {
+        if (value < 0) return PS_ERR_ARG;
+        g_tune.rounds_min_bytes = value;
+    } else {
+        return PS_ERR_ARG;
+    }
+    return PS_OK;
+}
+
+int64_t ps_get_tuning(const char *key) {
+    if (!key) return -1;
+    if (!std::strcmp(key, "scan_kernel")) return g_tune.scan_kernel;
+    if (!std::strcmp(key, "round_bytes")) return g_tune.round_bytes;
+    if (!std::strcmp(key, "rounds_min_bytes")) return g_tune.rounds_min_bytes;
+    if (!std::strcmp(key, "round_lead")) return g_tune.round_lead;
+    return -1;
 }
 
 int ps_scan(const void *in, void *out, int64_t n, int dtype_in, int dtype_out, int exclusive, uint64_t seed_bits,

@@ -118,9 +118,22 @@ __device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t ep
 // valid, so older stragglers never stall a tile whose neighbour is done.
 // The window slides back 32 tiles when it holds no P.  Tiles before `head`
 // read as P with value 0 (the head tile publishes P itself).
+#ifdef PS_TRACE
+__device__ uint64_t *g_trace;   // development builds only (scripts/trace*.cu)
+__device__ uint64_t *g_trace2;
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <typename A>
 __device__ A lookback(const Desc &d, int64_t tile, int64_t head, uint32_t epoch, int lane) {
     const uint64_t want = (uint64_t)epoch << 2;
+#ifdef PS_TRACE
+    uint32_t n_windows = 0, n_polls = 0;
+#endif
     A excl = (A)0;
     int64_t base = tile - 1;
     while (true) {
@@ -136,12 +149,19 @@ __device__ A lookback(const Desc &d, int64_t tile, int64_t head, uint32_t epoch,
             need = pmask ? ((pmask & (0u - pmask)) - 1) : FULL;  // lanes before the first P
             if ((xmask & need) == 0) break;
             if (++polls > 8) __nanosleep(polls > 64 ? 128 : 32);
+#ifdef PS_TRACE
+            ++n_polls;
+#endif
             if (!ok && ((need >> lane) & 1)) v = ld_desc(d.d + p);
         }
         const int first_p = pmask ? __ffs(pmask) - 1 : 32;
         A val = (A)0;
         if (live && lane <= first_p) val = acc_from_bits<A>(v.y);
         excl += warp_sum(val);
+#ifdef PS_TRACE
+        ++n_windows;
+        if (pmask && g_trace && lane == 0) g_trace[tile * 8 + 5] = ((uint64_t)n_windows << 32) | n_polls;
+#endif
         if (pmask) return excl;
         base -= 32;
     }

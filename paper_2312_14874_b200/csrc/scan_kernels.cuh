@@ -97,6 +97,14 @@ __global__ void __launch_bounds__(WARPS * 32)
     const TIn *in = reinterpret_cast<const TIn *>(a.in) + row * a.ld_in - a.lead + t0;
     TOut *out = reinterpret_cast<TOut *>(a.out) + row * a.ld_out - a.lead + t0;
     const bool full = a.vec_ok && t0 >= lo && t0 + TILE <= hi;
+#ifdef PS_TRACE
+    if (g_trace && threadIdx.x == 0) {
+        g_trace[tile * 8 + 0] = gtimer();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace[tile * 8 + 6] = smid;
+    }
+#endif
 
     // ---- load: ROWS independent 256-bit loads per thread --------------------------
     TIn x[ROWS][VEC];
@@ -152,7 +160,13 @@ __global__ void __launch_bounds__(WARPS * 32)
         wrun += rtot;
     }
     if (lane == 0) s_warp[warp] = wrun;
+#ifdef PS_TRACE
+    if (g_trace && threadIdx.x == 0) g_trace[tile * 8 + 1] = gtimer();
+#endif
     __syncthreads();
+#ifdef PS_TRACE
+    if (g_trace && threadIdx.x == 0) g_trace[tile * 8 + 2] = gtimer();
+#endif
 
     // ---- warp 0: tile aggregate, publish, look-back, publish inclusive -------------
     if (warp == 0) {
@@ -197,6 +211,9 @@ __global__ void __launch_bounds__(WARPS * 32)
             reinterpret_cast<A *>(a.totals)[row] = excl + agg;
     }
     __syncthreads();
+#ifdef PS_TRACE
+    if (g_trace && threadIdx.x == 0) g_trace[tile * 8 + 3] = gtimer();
+#endif
 
     // ---- add carries, convert, store -----------------------------------------------
     const A wbase = s_base[warp];
@@ -234,6 +251,9 @@ __global__ void __launch_bounds__(WARPS * 32)
             }
         }
     }
+#ifdef PS_TRACE
+    if (g_trace && threadIdx.x == 0) g_trace[tile * 8 + 4] = gtimer();
+#endif
 }
 
 // ---- deterministic read-only reduction ------------------------------------------------

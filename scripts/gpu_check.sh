@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 ./scripts/sweep > gpurun_out/sweep.log 2>&1; echo "sweep rc=$?"; cat gpurun_out/sweep.log
-timeout 1500 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-grep -E "FAILED|passed|failed" gpurun_out/pytest_gpu.log | tail -30
+for i in 1 2 3; do
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -x --timeout 600 -k "both_scan_kernels or rounds" > gpurun_out/pytest_rounds.log 2>&1; echo "pytest-rounds rc=$?"
+grep -E "FAILED|passed|failed|Error" gpurun_out/pytest_rounds.log | head -5
+done
+timeout 300 ./scripts/sweep > gpurun_out/sweep.log 2>&1; echo "sweep rc=$?"; grep -E "lookback|lead=2" gpurun_out/sweep.log

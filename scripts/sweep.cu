@@ -1,77 +1,76 @@
-// scripts/sweep.cu -- tile-geometry / look-back timing sweep of scan_tiles_kernel
-// on one GPU (development tool; not part of the library).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o scripts/sweep scripts/sweep.cu
+// scripts/sweep.cu -- kernel / geometry timing sweep through the public C-ABI
+// (development tool; not part of the library).  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o scripts/sweep scripts/sweep.cu \
+//        -Lpaper_2312_14874_b200 -lprefixscan_b200 -Xlinker -rpath='$ORIGIN/../paper_2312_14874_b200'
+#include <cuda_runtime.h>
+
 #include <cstdio>
 #include <cstdlib>
-#include <vector>
+#include <cstring>
 
-#include "../paper_2312_14874_b200/csrc/scan_kernels.cuh"
-
-using namespace ps;
+#include "../include/prefixscan_b200.h"
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
+#define PK(x) do { int rc = (x); if (rc) { printf("ps error %d (%s) at %d\n", rc, ps_error_string(rc), __LINE__); exit(1); } } while (0)
 
-__global__ void copy256(const V256 *in, V256 *out, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        stg256_stream(out + i, ldg256_stream(in + i));
-}
+static void *g_scratch;
+static size_t g_scratch_bytes;
+static uint32_t g_epoch;
 
-template <typename TIn, typename TOut, int WARPS, int ROWS>
-void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32_t &epoch, int flags, int reps) {
-    constexpr int64_t TILE = (int64_t)WARPS * ROWS * 32 * (32 / sizeof(TIn));
-    ScanArgs a{};
-    a.in = in; a.out = out; a.rows = 1; a.cols = n; a.ld_in = n; a.ld_out = n;
-    a.tiles_per_row = (n + TILE - 1) / TILE; a.vec_ok = 1; a.debug_flags = flags;
-    char *p = (char *)scratch;
-    a.desc.d = (ulonglong2 *)(p + 256);
-    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int w = 0; w < 3; ++w) { a.epoch = ++epoch; scan_tiles_kernel<TIn, TOut, WARPS, ROWS><<<(unsigned)a.tiles_per_row, WARPS * 32>>>(a); }
+static double time_scan(const void *in, void *out, int64_t n, int di, int dout, int excl, int reps) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int w = 0; w < 3; ++w)
+        PK(ps_scan(in, out, n, di, dout, excl, 0, nullptr, 0, nullptr, g_scratch, g_scratch_bytes, ++g_epoch, nullptr));
     CK(cudaDeviceSynchronize());
     cudaEventRecord(e0);
-    for (int r = 0; r < reps; ++r) { a.epoch = ++epoch; scan_tiles_kernel<TIn, TOut, WARPS, ROWS><<<(unsigned)a.tiles_per_row, WARPS * 32>>>(a); }
+    for (int r = 0; r < reps; ++r)
+        PK(ps_scan(in, out, n, di, dout, excl, 0, nullptr, 0, nullptr, g_scratch, g_scratch_bytes, ++g_epoch, nullptr));
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
-    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_tiles_kernel<TIn, TOut, WARPS, ROWS>, WARPS * 32, 0);
-    double gbs = (double)n * (sizeof(TIn) + sizeof(TOut)) / (ms * 1e-3) / 1e9;
-    printf("%-10s W=%2d R=%d tile=%6lld occ=%d lookback=%s  %8.1f us  %7.1f GB/s\n", name, WARPS, ROWS, (long long)TILE,
-           occ, (flags & 1) ? "off" : "on ", ms * 1e3, gbs);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms / reps;
 }
 
-template <typename TIn, typename TOut>
-void family(const char *name, int64_t n, void *in, void *out, void *scratch, uint32_t &epoch) {
-    for (int f : {0, 1}) {
-        run<TIn, TOut, 4, 4>(name, in, out, n, scratch, epoch, f, 20);
-        run<TIn, TOut, 8, 2>(name, in, out, n, scratch, epoch, f, 20);
-        run<TIn, TOut, 8, 4>(name, in, out, n, scratch, epoch, f, 20);
-        run<TIn, TOut, 8, 8>(name, in, out, n, scratch, epoch, f, 20);
-        run<TIn, TOut, 16, 2>(name, in, out, n, scratch, epoch, f, 20);
-        run<TIn, TOut, 16, 4>(name, in, out, n, scratch, epoch, f, 20);
-    }
-}
+struct Case {
+    const char *name;
+    int64_t n;
+    int di, dout, excl, ei, eo;
+};
 
-int main() {
-    const int64_t bytes = 1ll << 31;  // 2 GiB per buffer
-    void *in, *out, *scratch;
-    CK(cudaMalloc(&in, bytes)); CK(cudaMalloc(&out, bytes)); CK(cudaMalloc(&scratch, 256 << 20));
-    CK(cudaMemset(in, 0, bytes)); CK(cudaMemset(scratch, 0, 256 << 20));
-    uint32_t epoch = 0;
-    {
-        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-        int64_t nv = (1ll << 30) / 32;  // 1 GiB copy
-        for (int g : {148 * 4, 148 * 8, 148 * 16}) {
-            copy256<<<g, 256>>>((V256 *)in, (V256 *)out, nv);
-            cudaEventRecord(e0);
-            for (int r = 0; r < 20; ++r) copy256<<<g, 256>>>((V256 *)in, (V256 *)out, nv);
-            cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
-            float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 20;
-            printf("copy256 grid=%d  %8.1f us  %7.1f GB/s\n", g, ms * 1e3, 2.0 * (1 << 30) / (ms * 1e-3) / 1e9);
-        }
+int main(int argc, char **argv) {
+    const int64_t bytes = 1ll << 32;  // 4 GiB per buffer
+    void *in, *out;
+    CK(cudaMalloc(&in, bytes));
+    CK(cudaMalloc(&out, bytes));
+    CK(cudaMemset(in, 0, bytes));
+    g_scratch_bytes = 256 << 20;
+    CK(cudaMalloc(&g_scratch, g_scratch_bytes));
+    CK(cudaMemset(g_scratch, 0, g_scratch_bytes));
+    Case cases[] = {
+        {"cfg1 i64", 1ll << 24, PS_DTYPE_INT64, PS_DTYPE_INT64, 0, 8, 8},
+        {"cfg2 f32", 1ll << 28, PS_DTYPE_FLOAT32, PS_DTYPE_FLOAT32, 0, 4, 4},
+        {"cfg3 i32>i64 ex", 1ll << 28, PS_DTYPE_INT32, PS_DTYPE_INT64, 1, 4, 8},
+        {"2^28 i64", 1ll << 28, PS_DTYPE_INT64, PS_DTYPE_INT64, 0, 8, 8},
+    };
+    const int64_t rbs[] = {24ll << 20, 32ll << 20, 40ll << 20, 48ll << 20, 56ll << 20, 64ll << 20};
+    for (const Case &c : cases) {
+        PK(ps_set_tuning("scan_kernel", 1));
+        double ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
+        double gb = (double)c.n * (c.ei + c.eo) / 1e9;
+        printf("%-16s lookback            %8.1f us %7.1f GB/s\n", c.name, ms * 1e3, gb / (ms * 1e-3));
+        PK(ps_set_tuning("scan_kernel", 2));
+        for (int lead : {2})
+            for (int64_t rb : rbs) {
+                if (rb * (lead + 1) > (192ll << 20)) continue;
+                PK(ps_set_tuning("round_bytes", rb));
+                PK(ps_set_tuning("round_lead", lead));
+                ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
+                printf("%-16s rounds lead=%d R=%3lld MiB %8.1f us %7.1f GB/s\n", c.name, lead, (long long)(rb >> 20),
+                       ms * 1e3, gb / (ms * 1e-3));
+            }
     }
-    family<float, float>("cfg2 f32", 1ll << 28, in, out, scratch, epoch);
-    family<int64_t, int64_t>("cfg1 i64", 1ll << 24, in, out, scratch, epoch);
-    family<int64_t, int64_t>("2^27 i64", 1ll << 27, in, out, scratch, epoch);
-    family<int32_t, int64_t>("cfg3 i32", 1ll << 28, in, out, scratch, epoch);
     return 0;
 }

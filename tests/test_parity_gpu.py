@@ -218,6 +218,76 @@ def test_unaligned_starts(ps, dt):
             assert np.array_equal(_host(x)[s_in + n:], base[s_in + n:])
 
 
+@pytest.fixture
+def force_kernel():
+    """Pin the scan kernel (1 look-back, 2 cache-partitioned rounds) and a small
+    L2 region so modest inputs still span many regions; restore afterwards."""
+    from paper_2312_14874_b200 import _lib
+    lib = _lib.load()
+    saved = {k: lib.ps_get_tuning(k.encode()) for k in ("scan_kernel", "round_bytes", "rounds_min_bytes")}
+
+    def pin(kernel, round_bytes=1 << 20):
+        assert lib.ps_set_tuning(b"scan_kernel", kernel) == 0
+        assert lib.ps_set_tuning(b"round_bytes", round_bytes) == 0
+
+    yield pin
+    for k, v in saved.items():
+        lib.ps_set_tuning(k.encode(), v)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("dt", [np.int64, np.float32, np.uint32, np.int32, np.float64])
+def test_both_scan_kernels(ps, force_kernel, kernel, dt):
+    from paper_2312_14874_b200 import device
+    force_kernel(kernel)
+    r = np.random.default_rng(21)
+    for n in (1, 1000, 65_536, 1_000_003, 5_000_011):
+        x = GENS[dt](r, n + 9)
+        for s_in in (0, 3):
+            for exclusive in (False, True):
+                xs = x[s_in:s_in + n]
+                t = _cuda(x)[s_in:s_in + n]
+                o = torch.empty(x.shape[0], dtype=t.dtype, device="cuda")[s_in:s_in + n]
+                seed = 5 if x.dtype.kind != "f" else 0.25
+                tot = device.scan(t, o, exclusive=exclusive, seed=seed)
+                ctx = f"kernel={kernel} {dt.__name__} n={n} s={s_in} excl={exclusive}"
+                _assert_array(_host(o), _expected(xs, seed, exclusive), ctx)
+                tv = tot.cpu()
+                if x.dtype.kind == "f":
+                    assert abs(tv.item() - (xs.astype(np.float64).sum() + seed)) <= 1e-9 * n + 1e-9, ctx
+                elif dt == np.uint32:
+                    assert int(tv.view(torch.int64).item()) == int(xs.astype(np.uint64).sum()) + 5, ctx
+                else:
+                    assert int(tv.item()) == int(xs.astype(np.int64).sum()) + 5, ctx
+
+
+def test_rounds_kernel_widening_and_chaining(ps, force_kernel):
+    from paper_2312_14874_b200 import device
+    force_kernel(2)
+    flags = np.random.default_rng(2).integers(0, 2, 3_000_017, dtype=np.int32)
+    out = torch.empty(flags.shape[0], dtype=torch.int64, device="cuda")
+    tot = device.scan(_cuda(flags), out, exclusive=True, seed_terms=torch.tensor([7, 8], device="cuda"))
+    exp = np.concatenate([[0], np.cumsum(flags[:-1], dtype=np.int64)]) + 15
+    assert np.array_equal(_host(out), exp)
+    assert int(tot.item()) == int(flags.sum()) + 15
+    x = np.random.default_rng(3).random(2_000_000, dtype=np.float32)
+    t = _cuda(x)
+    device.scan(t)  # in place through the TMA ring
+    assert np.array_equal(_host(t), np.cumsum(x.astype(np.float64)).astype(np.float32))
+
+
+def test_rounds_kernel_is_deterministic(ps, force_kernel):
+    from paper_2312_14874_b200 import device
+    force_kernel(2)
+    x = _cuda(np.random.default_rng(4).standard_normal(4_000_037).astype(np.float32))
+    outs = []
+    for _ in range(3):
+        o = torch.empty_like(x)
+        device.scan(x, o)
+        outs.append(_host(o))
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
 def test_seed_terms_and_total_chaining(ps):
     """Chunked scans seeded with the previous chunk's device total equal one scan
     (the pattern the multi-GPU carry and the host pipeline rely on)."""
