@@ -133,7 +133,8 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
                   uint32_t epoch, cudaStream_t s) {
     using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
     int64_t G, portion, rounds;
-    if (!rounds_plan<TIn, TOut>(lead + n, G, portion, rounds)) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
+    if (!rounds_plan<TIn, TOut>(lead + n, G, portion, rounds) || G > 1024)
+        return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
     if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
     RoundArgs a{};
     a.in = static_cast<const TIn *>(in) - lead;
@@ -337,10 +338,11 @@ size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     if (!pair_ok(dtype_in, dtype_out) || n < 0) return 0;
     const int64_t tile = tile_of_dtype(dtype_in);
     size_t bytes = desc_bytes((n + tile - 1) / tile + 1);  // +1: a misaligned start can add a tile
-    // the cache-partitioned kernel needs one descriptor per (region, CTA); its
-    // grid is at most 8 CTAs per SM and regions are >= 1 MiB of input
-    const int64_t regions = (n * (int64_t)dsize(dtype_in)) / (1ll << 20) + 2;
-    const size_t rb = 256 + (size_t)regions * 8 * 160 * 16;
+    // the cache-partitioned kernel needs one descriptor per (region, CTA): at most
+    // 1024 persistent CTAs, regions of g_tune.round_bytes of input + output
+    const int64_t traffic = n * (int64_t)(dsize(dtype_in) + dsize(dtype_out));
+    const int64_t regions = traffic / g_tune.round_bytes + 2;
+    const size_t rb = 256 + (size_t)regions * 1024 * 16;
     return bytes > rb ? bytes : rb;
 }
 
