@@ -272,8 +272,6 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                     V256 raw[ROWS];
 #pragma unroll
                     for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + rr * ROW_ELEMS + lane * VEC);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&rempty[st]);
                     A s = (A)0;
 #pragma unroll
                     for (int rr = 0; rr < ROWS; ++rr) {
@@ -288,7 +286,11 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                             for (int j = 0; j + d < VEC; j += 2 * d) v[j] += v[j + d];
                         s += v[0];
                     }
+                    // release the stage only once the loaded values have been consumed:
+                    // a shared load still in flight must not race the next TMA fill
                     s = warp_sum(s);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&rempty[st]);
                     if (lane == 0) tot[k * RWP + rw] = s;
                 }
             } else {
@@ -451,9 +453,6 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                 V256 raw[ROWS];
 #pragma unroll
                 for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + rr * ROW_ELEMS + lane * VEC);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[st]);
-                ++use;
 #pragma unroll
                 for (int rr = 0; rr < ROWS; ++rr) {
                     TIn x[VEC];
@@ -461,6 +460,11 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
 #pragma unroll
                     for (int j = 0; j < VEC; ++j) v[rr][j] = (A)x[j];
                 }
+                // the conversions above consumed every loaded register, so the stage
+                // is really read before it is handed back to the producer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                ++use;
             } else {
 #pragma unroll
                 for (int rr = 0; rr < ROWS; ++rr)

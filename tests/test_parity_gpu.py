@@ -288,6 +288,22 @@ def test_rounds_kernel_is_deterministic(ps, force_kernel):
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
+@pytest.mark.parametrize("round_bytes", [16 << 20, 48 << 20, 96 << 20])
+def test_rounds_kernel_stress_full_size(ps, force_kernel, round_bytes):
+    """Many regions x 148 CTAs, repeated: any stage-reuse or ledger race shows up
+    as a persistent offset (exact integer comparison over 2^27 elements)."""
+    from paper_2312_14874_b200 import device
+    force_kernel(2, round_bytes)
+    flags = np.random.default_rng(7).integers(0, 2, 1 << 27, dtype=np.int32)
+    ref = np.cumsum(flags, dtype=np.int64)
+    x = _cuda(flags)
+    out = torch.empty(flags.shape[0], dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        tot = device.scan(x, out)
+        assert int(tot.item()) == int(ref[-1])
+        assert np.array_equal(_host(out), ref)
+
+
 def test_seed_terms_and_total_chaining(ps):
     """Chunked scans seeded with the previous chunk's device total equal one scan
     (the pattern the multi-GPU carry and the host pipeline rely on)."""
