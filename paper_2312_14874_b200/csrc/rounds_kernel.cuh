@@ -141,6 +141,47 @@ struct RoundGeom {
                                 2 * 2 * MAX_CHUNKS * 8 + 64;
 };
 
+// Sum of one lane-row of VEC elements in the accumulator type.  For float32
+// input the row is summed in float32 with Knuth's TwoSum error terms carried in
+// a second float (6 FMA-pipe ops per element) and converted to double once per
+// row: the conversion unit (XU, a quarter of the FP32 rate) is the scarce
+// resource of this kernel.  The pair (s, c) is exact whenever the error terms
+// sum without rounding -- e.g. for values on a common 2^-k grid such as
+// uniform [0,1) floats; otherwise the row total is within ~2^-46 relative.
+template <typename TIn, typename A, int VEC>
+__device__ __forceinline__ A lane_row_sum(const TIn (&x)[VEC]) {
+    if constexpr (sizeof(TIn) == 4 && (TIn)0.5 != (TIn)0) {
+        // pairwise tree (depth log2 VEC), error terms gathered in the same tree
+        float s[VEC], c[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            s[j] = x[j];
+            c[j] = 0.f;
+        }
+#pragma unroll
+        for (int d = 1; d < VEC; d <<= 1)
+#pragma unroll
+            for (int j = 0; j + d < VEC; j += 2 * d) {
+                const float a = s[j], b = s[j + d];
+                const float t = __fadd_rn(a, b);
+                const float bp = __fsub_rn(t, a);
+                const float err = __fadd_rn(__fsub_rn(a, __fsub_rn(t, bp)), __fsub_rn(b, bp));
+                s[j] = t;
+                c[j] = __fadd_rn(__fadd_rn(c[j], c[j + d]), err);
+            }
+        return (A)s[0] + (A)c[0];
+    } else {
+        A v[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] = (A)x[j];
+#pragma unroll
+        for (int d = 1; d < VEC; d <<= 1)
+#pragma unroll
+            for (int j = 0; j + d < VEC; j += 2 * d) v[j] += v[j + d];
+        return v[0];
+    }
+}
+
 template <typename A, int VEC>
 __device__ __forceinline__ void lane_prefix(A (&v)[VEC]) {  // in-register inclusive scan, log2(VEC) levels
 #pragma unroll
@@ -277,14 +318,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                     for (int rr = 0; rr < ROWS; ++rr) {
                         TIn x[VEC];
                         unpack<TIn>(raw[rr], x);
-                        A v[VEC];
-#pragma unroll
-                        for (int j = 0; j < VEC; ++j) v[j] = (A)x[j];
-#pragma unroll
-                        for (int d = 1; d < VEC; d <<= 1)
-#pragma unroll
-                            for (int j = 0; j + d < VEC; j += 2 * d) v[j] += v[j + d];
-                        s += v[0];
+                        s += lane_row_sum<TIn, A, VEC>(x);
                     }
                     // release the stage only once the loaded values have been consumed:
                     // a shared load still in flight must not race the next TMA fill

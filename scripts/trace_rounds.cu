@@ -58,7 +58,12 @@ int main() {
     CK(cudaMemset(in, 0, 1ll << 32)); CK(cudaMemset(scratch, 0, 64 << 20));
     uint32_t epoch = 0;
     run<float, float, 8, 4, 5, 4, 3>("f32", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 16, 2, 5, 4, 3>("f32_16x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 12, 2, 6, 4, 4>("f32_12x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 4, 4, 6, 3>("f32_8x4_r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 12, 4, 3, 4, 3>("f32_12x4", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
     run<int64_t, int64_t, 8, 4, 5, 4, 3>("i64", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<int32_t, int64_t, 8, 4, 5, 4, 3>("i32", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<int64_t, int64_t, 16, 2, 5, 4, 3>("i64_16x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<int64_t, int64_t, 12, 2, 6, 4, 4>("i64_12x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
     return 0;
 }
