@@ -242,11 +242,25 @@ def measured_peak():
 
 
 def committed_traffic(config_name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    launch list (profiles/traffic.json, written by scripts/summarize_ncu.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(config_name)
+            entry = json.load(fh).get(config_name)
+        return None if entry is None else float(entry["dram_bytes_per_launch"])
     except Exception:
         return None
+
+
+def dominant_kernel(lib, cfg, esize_in):
+    """Which kernel ps_scan / ps_scan_batched dispatches for this workload."""
+    if "rows" in cfg:
+        return "scan_tiles_kernel (batched rows, decoupled look-back)"
+    kern = lib.ps_get_tuning(b"scan_kernel")
+    big = cfg["n"] * esize_in >= lib.ps_get_tuning(b"rounds_min_bytes")
+    if kern == 2 or (kern == 0 and big):
+        return "scan_rounds_kernel (cache-partitioned accumulate-scan over L2 regions)"
+    return "scan_tiles_kernel (single-pass decoupled look-back)"
 
 
 def run_ours(args, cfg, cfg_name):
@@ -372,7 +386,7 @@ def run_ours(args, cfg, cfg_name):
             "hbm_frac_nominal": achieved / NOMINAL_HBM_GBS,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "scan_tiles_kernel", "kernel_avg_ms": kernel_ms,
+                         "kernel": dominant_kernel(_lib.load(), cfg, esize_in), "kernel_avg_ms": kernel_ms,
                          "algorithmic_bytes_per_launch": bytes_per_launch},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps, "parity": parity,

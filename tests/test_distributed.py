@@ -1,0 +1,150 @@
+"""Multi-process (gloo, CPU) tests of the sharded scan's host logic.
+
+The product's local operations are CUDA kernels; here they are replaced by
+the C oracle (test-only OracleOps) so the shard split, the all-gather of the
+shard totals, the carry fold and both schemes (reduce-then-scan =
+ACCUMULATE_SCAN_EQUAL, scan-then-fixup = SCAN_INCREMENT_EQUAL) run on CPU
+processes exactly as they do one-process-per-GPU under torchrun + NCCL.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+class OracleOps:
+    """Local ops on CPU tensors through the C oracle (test infrastructure)."""
+
+    def __init__(self):
+        from oracle import oracle
+        self.o = oracle
+
+    @staticmethod
+    def _acc(x):
+        return torch.float64 if x.dtype.is_floating_point else torch.int64
+
+    def reduce(self, x, seed=0):
+        a = x.numpy()
+        tot = self.o.accumulate(a, 0, a.shape[0]) + seed
+        return torch.tensor([tot], dtype=self._acc(x))
+
+    def scan(self, x, out, exclusive=False, seed=0, seed_terms=None):
+        s = seed + (seed_terms.sum().item() if seed_terms is not None else 0)
+        a = x.numpy().copy()
+        tot = self.o.scan(a, 0, a.shape[0], s)
+        if exclusive:
+            res = np.concatenate([[s], a[:-1]]).astype(a.dtype) if a.shape[0] else a
+        else:
+            res = a
+        out.copy_(torch.from_numpy(res))
+        return torch.tensor([tot], dtype=self._acc(x))
+
+    def add_offset(self, x, delta=0, delta_terms=None):
+        d = delta + (delta_terms.sum().item() if delta_terms is not None else 0)
+        a = x.numpy().copy()
+        self.o.increment(a, 0, a.shape[0], d)
+        x.copy_(torch.from_numpy(a))
+
+
+CASES = [(d, excl, seed) for d in ("int64", "float32") for excl, seed in ((False, 0), (True, 7))]
+N = 100_003
+
+
+def _global_input(dtype_name):
+    rng = np.random.default_rng(123)
+    if dtype_name == "int64":
+        return rng.integers(0, 1001, N, dtype=np.int64)
+    return rng.random(N, dtype=np.float32)
+
+
+def _worker(rank, world, port, scheme_name, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_14874_b200.distributed import ShardedScan, shard_span
+        from paper_2312_14874_b200.plan import SchemeId
+
+        results = []
+        for dtype_name, exclusive, seed in CASES:
+            g = _global_input(dtype_name)
+            sp = shard_span(N, world, rank, g.dtype.itemsize)
+            shard = torch.from_numpy(g[sp.start:sp.end].copy())
+            out = torch.empty_like(shard)
+            res = ShardedScan(scheme=SchemeId(scheme_name), ops=OracleOps())(shard, out, exclusive=exclusive,
+                                                                            seed=seed)
+            results.append((sp.start, sp.len, out.numpy(), res.total.item()))
+        parts = [None] * world
+        dist.all_gather_object(parts, results)
+        if rank == 0:
+            q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, scheme_name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, scheme_name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return parts
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("scheme", ["accumulate-scan", "scan-increment"])
+def test_sharded_scan_matches_global_scan(world, scheme):
+    parts = _run(world, scheme)
+    for ci, (dtype_name, exclusive, seed) in enumerate(CASES):
+        g = _global_input(dtype_name)
+        inc = np.cumsum(g.astype(np.float64 if dtype_name == "float32" else np.int64)) + seed
+        want = np.concatenate([[seed], inc[:-1]]) if exclusive else inc
+        mine = sorted((p[ci] for p in parts), key=lambda r: r[0])
+        got = np.concatenate([r[2] for r in mine])
+        assert sum(r[1] for r in mine) == N  # exact cover
+        ctx = f"{world} ranks {scheme} {dtype_name} excl={exclusive}"
+        if dtype_name == "int64":
+            assert np.array_equal(got, want.astype(np.int64)), ctx
+            assert all(int(r[3]) == int(inc[-1]) for r in mine), ctx
+        else:
+            rel = np.abs(got.astype(np.float64) - want) / np.maximum(np.abs(want), 1e-30)
+            assert rel.max() <= 1e-6, ctx
+            assert all(abs(r[3] - inc[-1]) <= 1e-9 * inc[-1] for r in mine), ctx
+
+
+def test_shard_span_exact_cover_and_alignment():
+    from paper_2312_14874_b200.distributed import shard_span
+    for n in (0, 1, 7, 100, 4096, 10**6 + 3):
+        for world in (1, 2, 3, 8):
+            spans = [shard_span(n, world, r, 8) for r in range(world)]
+            assert sum(s.len for s in spans) == n
+            pos = 0
+            for s in spans:
+                assert s.start == pos
+                pos += s.len
+            if n >= world * 4:
+                for s in spans[:-1]:
+                    assert s.len % 4 == 0  # 32-byte vector alignment for int64
+
+
+def test_sharded_scan_rejects_plus_one_schemes():
+    from paper_2312_14874_b200.distributed import ShardedScan
+    from paper_2312_14874_b200.plan import SchemeId
+    with pytest.raises(ValueError):
+        ShardedScan(scheme=SchemeId.ACCUMULATE_SCAN_PLUS_ONE)
