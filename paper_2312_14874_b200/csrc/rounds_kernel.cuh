@@ -211,9 +211,15 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
     uint64_t *rempty = rfull + RSTAGES;
     A *chunk_tot = reinterpret_cast<A *>(rempty + RSTAGES);  // [2][MAXC] (region parity)
     A *chunk_pre = chunk_tot + 2 * MAXC;                      // [2][MAXC] starting carries
-    __shared__ volatile int s_reduced;    // regions whose chunk totals are in chunk_tot
-    __shared__ volatile int s_prefixed;   // regions whose carries are in chunk_pre
-    __shared__ volatile int s_done[SW];   // regions completed, per scanner warp
+    // role hand-offs are mbarriers, so waiting warps sleep in try_wait instead of
+    // spinning on shared flags and stealing issue slots from the scanners:
+    //   bar_red[r&1]   reducer -> ledger   chunk totals of region r written     (1 arrival)
+    //   bar_pre[r&1]   ledger  -> all      chunk carries of region r written    (1 arrival)
+    //   bar_scan[r&7]  scanners -> all     region r stored by every scanner warp (SW arrivals)
+    // Scanner warps drift apart by at most STAGES sub-tiles (the TMA ring), i.e.
+    // fewer than 8 regions, so arrivals for regions r and r+8 never share a phase.
+    static_assert(STAGES < 8, "bar_scan slots must exceed the scanner drift");
+    __shared__ __align__(8) uint64_t bar_red[2], bar_pre[2], bar_scan[8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
@@ -234,9 +240,11 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             mbar_init(&rempty[s], RWP);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_reduced = 0;
-        s_prefixed = 0;
-        for (int w = 0; w < SW; ++w) s_done[w] = 0;
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar_red[i], 1);
+            mbar_init(&bar_pre[i], 1);
+        }
+        for (int i = 0; i < 8; ++i) mbar_init(&bar_scan[i], SW);
     }
     __syncthreads();
 
@@ -252,17 +260,19 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
         const int64_t p0 = r * a.round_elems + (int64_t)c * a.portion;
         return p0 >= a.lo && p0 + a.portion <= a.hi;
     };
-    // regions every scanner warp has finished (warps drift apart by up to STAGES
-    // sub-tiles, which can be several small regions)
-    auto scanned_regions = [&]() {
-        int m = s_done[0];
-#pragma unroll
-        for (int w = 1; w < SW; ++w) m = min(m, (int)s_done[w]);
-        return m;
+    // wait until region q has been stored by every scanner warp / has its carries
+    // (q < 0: nothing to wait for).  Slot reuse is safe: a waiter for region q
+    // has already waited for region q-8 (q-2 for bar_pre).
+    auto wait_scanned = [&](int64_t q) {
+        if (q >= 0) mbar_wait(&bar_scan[q & 7], (uint32_t)((q >> 3) & 1));
+    };
+    auto wait_prefixed = [&](int64_t q) {
+        if (q >= 0) mbar_wait(&bar_pre[q & 1], (uint32_t)((q >> 1) & 1));
     };
     // L2 holds regions [r-lead, r]; chunk_tot[r&1] is free once the ledger used region r-2
-    auto reducer_may_start = [&](int64_t r) {
-        return scanned_regions() >= r - a.lead_regions && s_prefixed >= r - 1;
+    auto wait_reducer_may_start = [&](int64_t r) {
+        wait_scanned(r - a.lead_regions - 1);
+        wait_prefixed(r - 2);
     };
 
     if (warp == W_RPROD) {
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             uint32_t use = 0;
             for (int64_t r = 0; r < a.rounds; ++r) {
                 if (!whole_portion(r)) continue;
-                while (!reducer_may_start(r)) __nanosleep(128);
+                wait_reducer_may_start(r);
                 const int64_t p0 = r * a.round_elems + (int64_t)c * a.portion;
                 {
                     constexpr int64_t PIECE = 65536;
@@ -299,7 +309,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
         const int rw = warp - SW;
         uint32_t use = 0;
         for (int64_t r = 0; r < a.rounds; ++r) {
-            while (!reducer_may_start(r)) __nanosleep(128);
+            wait_reducer_may_start(r);
 #ifdef PS_TRACE
             if (g_trace && rw == 0 && lane == 0) g_trace[(r * G + c) * 8 + 0] = gtimer();
 #endif
@@ -320,9 +330,11 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                         unpack<TIn>(raw[rr], x);
                         s += lane_row_sum<TIn, A, VEC>(x);
                     }
-                    // release the stage only once the loaded values have been consumed:
-                    // a shared load still in flight must not race the next TMA fill
+                    // release the stage only once the loaded values have been consumed
+                    // (and behind a generic->async proxy fence): a shared load still in
+                    // flight must not race the next TMA fill
                     s = warp_sum(s);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&rempty[st]);
                     if (lane == 0) tot[k * RWP + rw] = s;
@@ -347,7 +359,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                 if (lane == 0) {
                     st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
                     __threadfence_block();
-                    s_reduced = (int)(r + 1);
+                    mbar_arrive(&bar_red[r & 1]);
 #ifdef PS_TRACE
                     if (g_trace) g_trace[(r * G + c) * 8 + 1] = gtimer();
 #endif
@@ -427,8 +439,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 2] = gtimer();
 #endif
             // own chunk totals ready, and the scanners are done with region r-2's carries
-            while (s_reduced < r + 1 || scanned_regions() < r - 1) __nanosleep(32);
-            __threadfence_block();
+            mbar_wait(&bar_red[r & 1], (uint32_t)((r >> 1) & 1));
+            wait_scanned(r - 2);
             const A *tot = chunk_tot + (r & 1) * MAXC;
             A *pre = chunk_pre + (r & 1) * MAXC;
             // exclusive scan of the chunk totals: lane owns a contiguous block of chunks
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             carry += sa;
             __syncwarp();
             __threadfence_block();
-            if (lane == 0) s_prefixed = (int)(r + 1);
+            if (lane == 0) mbar_arrive(&bar_pre[r & 1]);
 #ifdef PS_TRACE
             if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 3] = gtimer();
 #endif
@@ -465,8 +477,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
     const uint64_t pol_stream = policy_evict_first();
     uint32_t use = 0;
     for (int64_t r = 0; r < a.rounds; ++r) {
-        while (s_prefixed < r + 1) __nanosleep(32);
-        __threadfence_block();
+        wait_prefixed(r);
 #ifdef PS_TRACE
         if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
 #endif
@@ -494,10 +505,6 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
 #pragma unroll
                     for (int j = 0; j < VEC; ++j) v[rr][j] = (A)x[j];
                 }
-                // the conversions above consumed every loaded register, so the stage
-                // is really read before it is handed back to the producer
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[st]);
                 ++use;
             } else {
 #pragma unroll
@@ -508,12 +515,20 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
                         v[rr][j] = (pos >= a.lo && pos < a.hi) ? (A)in[pos] : (A)0;
                     }
             }
-            // exclusive outputs need the element itself: keep a copy of the last one only
-            A first[ROWS];
 #pragma unroll
             for (int rr = 0; rr < ROWS; ++rr) {
-                first[rr] = v[rr][0];
-                lane_prefix<A, VEC>(v[rr]);  // v[rr][j] = x0 + ... + xj
+#pragma unroll
+                for (int j = 1; j < VEC; ++j) v[rr][j] += v[rr][j - 1];  // x0 + ... + xj (rows give the ILP)
+            }
+            if (tma) {
+                // Hand the stage back only after every loaded value has been consumed
+                // (the row prefixes depend on all of them) and after a generic->async
+                // proxy fence: the next TMA fill of this stage must not overtake a
+                // shared load that is still in flight (observed for int64, where the
+                // widening is a no-op and nothing else waited on the loads).
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[(use - 1) % STAGES]);
             }
             A sc[ROWS];
 #pragma unroll
@@ -547,7 +562,6 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
 #pragma unroll
                     for (int j = 0; j < VEC; ++j) y[j] = (TOut)(b + v[rr][j]);
                 }
-                (void)first;
                 if (tma) {
                     constexpr int NV = VEC * sizeof(TOut) / 32;
 #pragma unroll
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             }
         }
         __syncwarp();
-        if (lane == 0) s_done[warp] = (int)(r + 1);
+        if (lane == 0) mbar_arrive(&bar_scan[r & 7]);
 #ifdef PS_TRACE
         if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
 #endif
