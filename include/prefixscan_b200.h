@@ -168,6 +168,8 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
  *                      2 = cache-partitioned rounds (persistent, L2 regions)
  *   "round_bytes"      input + output bytes per L2 region of the rounds kernel
  *   "round_lead"       regions the rounds kernel's reducer warps run ahead
+ *   "round_ramp"       ramp regions (halving sizes) at each end of the rounds kernel
+ *   "round_prefetch"   1 = bulk L2 prefetch of each reducer portion (rounds kernel)
  *   "rounds_min_bytes" auto mode uses the rounds kernel from this input size
  * Returns PS_ERR_ARG for an unknown key or value. */
 int ps_set_tuning(const char *key, int64_t value);

@@ -76,11 +76,20 @@ struct Tuning {
     int64_t round_bytes = 48ll << 20;       // input + output bytes per L2 region (rounds kernel)
     int64_t rounds_min_bytes = 16ll << 20;  // auto: rounds kernel from this many input bytes
     int64_t round_lead = 2;                 // regions the reducer warps may run ahead of the scanners
+    int64_t round_ramp = 0;                 // ramp regions at each end (sizes P/2^k .. P/2); 0 = off
+    int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)
 };
 Tuning g_tune;
 
 // rounds kernel: scanner warps, rows per warp, TMA stages, reducer warps, reducer lead (regions)
-constexpr int RW = 8, RR = 4, RS = 5, RRED = 4, RRS = 3;
+constexpr int RW = 8, RR = 4, RRED = 4;
+// shared-memory split between the scanner ring (L2 re-reads) and the reducer
+// ring (HBM reads): float32 rows need deeper reducer buffering (measured with
+// scripts/trace_rounds.cu), the rest favours the scanner ring
+template <typename TIn> struct RingSplit { static constexpr int RS = 5, RRS = 3; };
+template <> struct RingSplit<float> { static constexpr int RS = 3, RRS = 6; };
+#define RGEO RoundGeom<TIn, TOut, RW, RR, RingSplit<TIn>::RS, RRED, RingSplit<TIn>::RRS>
+#define RKERN scan_rounds_kernel<TIn, TOut, RW, RR, RingSplit<TIn>::RS, RRED, RingSplit<TIn>::RRS>
 
 struct DevInfo {
     int sms = 0;
@@ -97,8 +106,8 @@ int device_sms() {
 
 template <typename TIn, typename TOut>
 int rounds_grid() {
-    using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
-    auto kern = scan_rounds_kernel<TIn, TOut, RW, RR, RS, RRED, RRS>;
+    using Geo = RGEO;
+    auto kern = RKERN;
     static int per_sm[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -113,17 +122,38 @@ int rounds_grid() {
     return per_sm[dev] > 0 ? per_sm[dev] * device_sms() : 0;
 }
 
-// geometry of the rounds kernel for n positions: (G, portion, rounds)
+// geometry of the rounds kernel for n positions: grid, full-region portion,
+// ramp, full-region count and launched regions (see region_geom)
+struct RoundPlan {
+    int64_t G, portion, full, rounds;
+    int ramp;
+};
+
 template <typename TIn, typename TOut>
-bool rounds_plan(int64_t positions, int64_t &G, int64_t &portion, int64_t &rounds) {
-    using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
-    G = rounds_grid<TIn, TOut>();
-    if (G <= 0) return false;
-    int64_t want = g_tune.round_bytes / (int64_t)(sizeof(TIn) + sizeof(TOut)) / G;
-    portion = want / Geo::SUB * Geo::SUB;
-    if (portion < Geo::SUB) portion = Geo::SUB;
-    if (portion > (int64_t)Geo::MAX_CHUNKS * Geo::CHUNK) portion = (int64_t)Geo::MAX_CHUNKS * Geo::CHUNK / Geo::SUB * Geo::SUB;
-    rounds = (positions + portion * G - 1) / (portion * G);
+bool rounds_plan(int64_t positions, RoundPlan &p) {
+    using Geo = RGEO;
+    p.G = rounds_grid<TIn, TOut>();
+    if (p.G <= 0) return false;
+    p.ramp = (int)g_tune.round_ramp;
+    const int64_t unit = Geo::SUB;
+    int64_t want = g_tune.round_bytes / (int64_t)(sizeof(TIn) + sizeof(TOut)) / p.G;
+    p.portion = want / unit * unit;
+    if (p.portion < unit) p.portion = unit;
+    const int64_t cap = (int64_t)Geo::MAX_CHUNKS * Geo::CHUNK / unit * unit;
+    if (p.portion > cap) p.portion = cap;
+    const int64_t per_cta = (positions + p.G - 1) / p.G;
+    int64_t ramps = 0;
+    for (int k = 1; k <= p.ramp; ++k) ramps += 2 * ramp_part(p.portion, Geo::SUB, k);
+    p.full = per_cta > ramps ? (per_cta - ramps + p.portion - 1) / p.portion : 0;
+    // launch only regions that start before the end of the data
+    const int64_t total = 2 * (int64_t)p.ramp + p.full;
+    p.rounds = 0;
+    for (int64_t r = 0; r < total; ++r) {
+        int64_t start, part;
+        region_geom(p.portion, p.ramp, p.full, p.G, Geo::SUB, r, start, part);
+        if (start >= positions) break;
+        p.rounds = r + 1;
+    }
     return true;
 }
 
@@ -131,19 +161,20 @@ template <typename TIn, typename TOut>
 int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclusive, uint64_t seed_bits,
                   const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
                   uint32_t epoch, cudaStream_t s) {
-    using Geo = RoundGeom<TIn, TOut, RW, RR, RS, RRED, RRS>;
-    int64_t G, portion, rounds;
-    if (!rounds_plan<TIn, TOut>(lead + n, G, portion, rounds) || G > 1024)
-        return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
-    if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
+    using Geo = RGEO;
+    RoundPlan pl;
+    if (!rounds_plan<TIn, TOut>(lead + n, pl) || pl.G > 1024) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
+    const int64_t G = pl.G;
+    if (!scratch || scratch_bytes < 256 + (size_t)(pl.rounds * G) * 16) return PS_ERR_SCRATCH;
     RoundArgs a{};
     a.in = static_cast<const TIn *>(in) - lead;
     a.out = static_cast<TOut *>(out) - lead;
     a.lo = lead;
     a.hi = lead + n;
-    a.round_elems = portion * G;
-    a.portion = portion;
-    a.rounds = rounds;
+    a.portion = pl.portion;
+    a.rounds = pl.rounds;
+    a.full_regions = pl.full;
+    a.ramp = pl.ramp;
     a.seed_bits = seed_bits;
     a.seed_terms = seed_terms;
     a.n_seed_terms = n_seed_terms;
@@ -152,8 +183,9 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
     a.epoch = epoch;
     a.exclusive = exclusive;
     a.lead_regions = (int)g_tune.round_lead;
+    a.l2_prefetch = (int)g_tune.round_prefetch;
     void *params[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)scan_rounds_kernel<TIn, TOut, RW, RR, RS, RRED, RRS>,
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)RKERN,
                                                 dim3((unsigned)G), dim3(Geo::THREADS), params, Geo::SMEM, s);
     return cuda_rc(e);
 }
@@ -341,7 +373,7 @@ size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     // the cache-partitioned kernel needs one descriptor per (region, CTA): at most
     // 1024 persistent CTAs, regions of g_tune.round_bytes of input + output
     const int64_t traffic = n * (int64_t)(dsize(dtype_in) + dsize(dtype_out));
-    const int64_t regions = traffic / g_tune.round_bytes + 2;
+    const int64_t regions = traffic / g_tune.round_bytes + 2 + 2 * g_tune.round_ramp;
     const size_t rb = 256 + (size_t)regions * 1024 * 16;
     return bytes > rb ? bytes : rb;
 }
@@ -357,6 +389,12 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "round_lead")) {
         if (value < 1 || value > 8) return PS_ERR_ARG;
         g_tune.round_lead = value;
+    } else if (!std::strcmp(key, "round_prefetch")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.round_prefetch = value;
+    } else if (!std::strcmp(key, "round_ramp")) {
+        if (value < 0 || value > 4) return PS_ERR_ARG;
+        g_tune.round_ramp = value;
     } else if (!std::strcmp(key, "rounds_min_bytes")) {
         if (value < 0) return PS_ERR_ARG;
         g_tune.rounds_min_bytes = value;
@@ -372,6 +410,8 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "round_bytes")) return g_tune.round_bytes;
     if (!std::strcmp(key, "rounds_min_bytes")) return g_tune.rounds_min_bytes;
     if (!std::strcmp(key, "round_lead")) return g_tune.round_lead;
+    if (!std::strcmp(key, "round_ramp")) return g_tune.round_ramp;
+    if (!std::strcmp(key, "round_prefetch")) return g_tune.round_prefetch;
     return -1;
 }
 

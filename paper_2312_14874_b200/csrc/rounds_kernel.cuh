@@ -94,9 +94,10 @@ struct RoundArgs {
     const void *in;   // aligned base: position p <-> element p - lead
     void *out;
     int64_t lo, hi;   // valid positions [lo, hi) (lo = lead, hi = lead + n)
-    int64_t round_elems;  // R positions per region (multiple of G * SUB)
-    int64_t portion;      // P = R / G (multiple of SUB)
-    int64_t rounds;
+    int64_t portion;      // P: per-CTA positions of a full region (multiple of SUB << ramp)
+    int64_t rounds;       // regions actually launched (ramp-up + full + ramp-down, trailing empties dropped)
+    int64_t full_regions; // F full-size regions between the ramps
+    int ramp;             // K: regions 0..K-1 have portions P/2^K .. P/2, the K after the full ones P/2 .. P/2^K
     uint64_t seed_bits;
     const void *seed_terms;
     int64_t n_seed_terms;
@@ -105,7 +106,37 @@ struct RoundArgs {
     uint32_t epoch;
     int exclusive;
     int lead_regions;     // reducer runs up to this many regions ahead of the scanners
+    int l2_prefetch;      // issue a bulk L2 prefetch of each reducer portion
 };
+
+// Region r of the ramped schedule: first position and per-CTA portion.  Small
+// regions at both ends shorten the pipeline fill (first region reduced alone)
+// and drain (last region scanned alone).
+__host__ __device__ __forceinline__ int64_t ramp_part(int64_t P, int64_t sub, int k) {  // P/2^k, >= sub
+    const int64_t q = (P >> k) / sub * sub;
+    return q < sub ? sub : q;
+}
+__host__ __device__ __forceinline__ void region_geom(int64_t portion, int ramp, int64_t full, int64_t G, int64_t sub,
+                                                     int64_t r, int64_t &start, int64_t &part) {
+    const int64_t P = portion;
+    int64_t up = 0;  // ramp-up regions: P/2^ramp .. P/2 (multiples of sub)
+    for (int q = 0; q < ramp && q < r; ++q) up += ramp_part(P, sub, ramp - q);
+    if (r < ramp) {
+        part = ramp_part(P, sub, (int)(ramp - r));
+        start = G * up;
+        return;
+    }
+    if (r < ramp + full) {
+        part = P;
+        start = G * (up + (r - ramp) * P);
+        return;
+    }
+    const int64_t i = r - ramp - full;  // ramp-down: P/2, P/4, ...
+    int64_t down = 0;
+    for (int q = 0; q < i; ++q) down += ramp_part(P, sub, q + 1);
+    part = ramp_part(P, sub, (int)(i + 1));
+    start = G * (up + full * P + down);
+}
 
 __device__ __forceinline__ void named_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -226,9 +257,12 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
     const TIn *in = reinterpret_cast<const TIn *>(a.in);
     TOut *out = reinterpret_cast<TOut *>(a.out);
     const uint64_t want = (uint64_t)a.epoch << 2;
-    const int64_t nchunk = a.portion / CHUNK;  // <= MAXC (host guarantees)
-    const int64_t nsub = a.portion / SUB;
-    const int64_t nrsub = a.portion / RSUB;
+    // this CTA's portion of region r: [p0, p0 + part)
+    auto portion_of = [&](int64_t r, int64_t &p0, int64_t &part) {
+        int64_t start;
+        region_geom(a.portion, a.ramp, a.full_regions, G, SUB, r, start, part);
+        p0 = start + (int64_t)c * part;
+    };
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -239,26 +273,29 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             mbar_init(&rfull[s], 1);
             mbar_init(&rempty[s], RWP);
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_red[i], 1);
             mbar_init(&bar_pre[i], 1);
         }
         for (int i = 0; i < 8; ++i) mbar_init(&bar_scan[i], SW);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     // sub-tiles [k_lo, k_hi) of a region's portion are fully valid (scanner TMA path)
     auto span_of = [&](int64_t r, int64_t &p0, int64_t &k_lo, int64_t &k_hi) {
-        p0 = r * a.round_elems + (int64_t)c * a.portion;
+        int64_t part;
+        portion_of(r, p0, part);
+        const int64_t nsub = part / SUB;
         k_lo = a.lo <= p0 ? 0 : (a.lo - p0 + SUB - 1) / SUB;
         k_hi = a.hi <= p0 ? 0 : (a.hi - p0) / SUB;
         if (k_hi > nsub) k_hi = nsub;
         if (k_lo > k_hi) k_lo = k_hi;
     };
     auto whole_portion = [&](int64_t r) {
-        const int64_t p0 = r * a.round_elems + (int64_t)c * a.portion;
-        return p0 >= a.lo && p0 + a.portion <= a.hi;
+        int64_t p0, part;
+        portion_of(r, p0, part);
+        return p0 >= a.lo && p0 + part <= a.hi;
     };
     // wait until region q has been stored by every scanner warp / has its carries
     // (q < 0: nothing to wait for).  Slot reuse is safe: a waiter for region q
@@ -283,10 +320,12 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             for (int64_t r = 0; r < a.rounds; ++r) {
                 if (!whole_portion(r)) continue;
                 wait_reducer_may_start(r);
-                const int64_t p0 = r * a.round_elems + (int64_t)c * a.portion;
-                {
+                int64_t p0, part;
+                portion_of(r, p0, part);
+                const int64_t nrsub = part / RSUB;
+                if (a.l2_prefetch) {
                     constexpr int64_t PIECE = 65536;
-                    const int64_t bytes = a.portion * (int64_t)sizeof(TIn);
+                    const int64_t bytes = part * (int64_t)sizeof(TIn);
                     const char *src = reinterpret_cast<const char *>(in + p0);
                     for (int64_t o = 0; o < bytes; o += PIECE) {
                         const uint32_t sz = (uint32_t)((bytes - o) < PIECE ? (bytes - o) : PIECE);
@@ -314,7 +353,9 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             if (g_trace && rw == 0 && lane == 0) g_trace[(r * G + c) * 8 + 0] = gtimer();
 #endif
             A *tot = chunk_tot + (r & 1) * MAXC;
-            const int64_t p0 = r * a.round_elems + (int64_t)c * a.portion;
+            int64_t p0, part;
+            portion_of(r, p0, part);
+            const int64_t nrsub = part / RSUB, nchunk = part / CHUNK;
             if (whole_portion(r)) {
                 for (int64_t k = 0; k < nrsub; ++k, ++use) {
                     const uint32_t st = use % RSTAGES;
@@ -443,6 +484,9 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             wait_scanned(r - 2);
             const A *tot = chunk_tot + (r & 1) * MAXC;
             A *pre = chunk_pre + (r & 1) * MAXC;
+            int64_t p0r, part;
+            portion_of(r, p0r, part);
+            const int64_t nchunk = part / CHUNK;
             // exclusive scan of the chunk totals: lane owns a contiguous block of chunks
             const int64_t per = (nchunk + 31) / 32;
             const int64_t b0 = lane * per, b1 = (b0 + per) < nchunk ? (b0 + per) : nchunk;
@@ -482,8 +526,10 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
         if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
 #endif
         const A *pre = chunk_pre + (r & 1) * MAXC;
-        int64_t p0, k_lo, k_hi;
+        int64_t p0, k_lo, k_hi, part;
         span_of(r, p0, k_lo, k_hi);
+        portion_of(r, p0, part);
+        const int64_t nsub = part / SUB;
         for (int64_t k = 0; k < nsub; ++k) {
             const int64_t t0 = p0 + k * SUB + (int64_t)warp * CHUNK;  // this warp's chunk
             const int64_t sub0 = p0 + k * SUB;

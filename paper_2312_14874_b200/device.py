@@ -298,7 +298,7 @@ def wrapped_block_total(x: torch.Tensor, w: int, seed=0) -> torch.Tensor:
 
 
 # ---- host buffers: the end-to-end entry point ---------------------------------------------------
-DEFAULT_CHUNK_BYTES = 64 << 20
+DEFAULT_CHUNK_BYTES = 32 << 20  # measured best on PCIe Gen5 (scripts/e2e_sweep.py)
 
 
 class _HostWorkspace:

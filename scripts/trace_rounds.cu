@@ -21,8 +21,8 @@ void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32
     int64_t portion = round_bytes / (int64_t)sizeof(TIn) / G / Geo::SUB * Geo::SUB;
     if (portion < Geo::SUB) portion = Geo::SUB;
     RoundArgs a{};
-    a.in = in; a.out = out; a.lo = 0; a.hi = n; a.round_elems = portion * G; a.portion = portion; a.lead_regions = 2;
-    a.rounds = (n + a.round_elems - 1) / a.round_elems;
+    a.in = in; a.out = out; a.lo = 0; a.hi = n; a.portion = portion; a.lead_regions = 2; a.ramp = 0; a.l2_prefetch = 0;
+    a.rounds = (n + portion * G - 1) / (portion * G); a.full_regions = a.rounds;
     a.desc = (ulonglong2 *)((char *)scratch + 256);
     uint64_t *tr; size_t tb = (size_t)a.rounds * G * 64;
     CK(cudaMalloc(&tr, tb)); CK(cudaMemset(tr, 0, tb));
@@ -58,12 +58,12 @@ int main() {
     CK(cudaMemset(in, 0, 1ll << 32)); CK(cudaMemset(scratch, 0, 64 << 20));
     uint32_t epoch = 0;
     run<float, float, 8, 4, 5, 4, 3>("f32", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 16, 2, 5, 4, 3>("f32_16x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 12, 2, 6, 4, 4>("f32_12x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 8, 4, 4, 6, 3>("f32_8x4_r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 12, 4, 3, 4, 3>("f32_12x4", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 4, 3, 4, 6>("f32_s3r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 4, 4, 4, 5>("f32_s4r5", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<int64_t, int64_t, 8, 4, 5, 4, 3>("cfg1", in, out, 1ll << 24, scratch, epoch, 20ll << 20);
+    run<int64_t, int64_t, 8, 4, 3, 4, 6>("cfg1_s3r6", in, out, 1ll << 24, scratch, epoch, 20ll << 20);
+    run<int64_t, int64_t, 8, 4, 4, 4, 5>("cfg1_s4r5", in, out, 1ll << 24, scratch, epoch, 20ll << 20);
     run<int64_t, int64_t, 8, 4, 5, 4, 3>("i64", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<int64_t, int64_t, 16, 2, 5, 4, 3>("i64_16x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<int64_t, int64_t, 12, 2, 6, 4, 4>("i64_12x2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<int64_t, int64_t, 8, 4, 3, 4, 6>("i64_s3r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
     return 0;
 }
