@@ -165,8 +165,9 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
 
 /* Tuning knobs (process-wide; for benchmarks and tests):
  *   "scan_kernel"      0 = auto, 1 = single-pass decoupled look-back,
- *                      2 = cache-partitioned rounds (persistent, L2 regions)
- *   "round_bytes"      input + output bytes per L2 region of the rounds kernel
+ *                      2 = cache-partitioned rounds (persistent, L2 regions),
+ *                      3 = shared-memory-resident streaming regions (persistent)
+ *   "round_bytes"      input + output bytes per L2 region of the rounds kernel (0 = default)
  *   "round_lead"       regions the rounds kernel's reducer warps run ahead
  *   "round_ramp"       ramp regions (halving sizes) at each end of the rounds kernel
  *   "round_prefetch"   1 = bulk L2 prefetch of each reducer portion (rounds kernel)

@@ -14,6 +14,7 @@
 #include "segmented.cuh"
 #include "aux_kernels.cuh"
 #include "rounds_kernel.cuh"
+#include "stream_kernel.cuh"
 
 namespace ps {
 namespace {
@@ -73,7 +74,7 @@ bool overlaps_partially(const void *a, size_t abytes, const void *b, size_t bbyt
 // ---- tuning (ps_set_tuning) ----------------------------------------------------------------
 struct Tuning {
     int scan_kernel = 0;                    // 0 auto, 1 look-back, 2 cache-partitioned rounds
-    int64_t round_bytes = 48ll << 20;       // input + output bytes per L2 region (rounds kernel)
+    int64_t round_bytes = 0;                // input + output bytes per L2 region (0 = per-dtype default)
     int64_t rounds_min_bytes = 16ll << 20;  // auto: rounds kernel from this many input bytes
     int64_t round_lead = 2;                 // regions the reducer warps may run ahead of the scanners
     int64_t round_ramp = 0;                 // ramp regions at each end (sizes P/2^k .. P/2); 0 = off
@@ -122,6 +123,15 @@ int rounds_grid() {
     return per_sm[dev] > 0 ? per_sm[dev] * device_sms() : 0;
 }
 
+// Region size (input + output bytes) of the rounds kernel, measured with
+// scripts/sweep.cu: float32 rows are compute-heavier and prefer 48 MiB,
+// integer paths 64 MiB (a larger share of the L2 per region).
+template <typename TIn, typename TOut>
+int64_t region_bytes() {
+    if (g_tune.round_bytes > 0) return g_tune.round_bytes;
+    return (sizeof(TIn) == 4 && (TIn)0.5 != (TIn)0) ? (48ll << 20) : (64ll << 20);
+}
+
 // geometry of the rounds kernel for n positions: grid, full-region portion,
 // ramp, full-region count and launched regions (see region_geom)
 struct RoundPlan {
@@ -136,7 +146,7 @@ bool rounds_plan(int64_t positions, RoundPlan &p) {
     if (p.G <= 0) return false;
     p.ramp = (int)g_tune.round_ramp;
     const int64_t unit = Geo::SUB;
-    int64_t want = g_tune.round_bytes / (int64_t)(sizeof(TIn) + sizeof(TOut)) / p.G;
+    int64_t want = region_bytes<TIn, TOut>() / (int64_t)(sizeof(TIn) + sizeof(TOut)) / p.G;
     p.portion = want / unit * unit;
     if (p.portion < unit) p.portion = unit;
     const int64_t cap = (int64_t)Geo::MAX_CHUNKS * Geo::CHUNK / unit * unit;
@@ -190,6 +200,64 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
     return cuda_rc(e);
 }
 
+// ---- shared-memory-resident streaming kernel (stream_kernel.cuh) ---------------------------------
+constexpr int SSW = 8, SROWS = 4, SNBUF = 3, SRWP = 4;
+#define SGEO StreamGeom<TIn, SSW, SROWS, SNBUF, SRWP>
+#define SKERN scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP>
+
+template <typename TIn, typename TOut>
+int64_t stream_portion() {  // positions per CTA per region: NBUF buffers in ~200 KB
+    constexpr int64_t unit = (int64_t)SSW * SGEO::CHUNK;
+    int64_t p = (int64_t)SGEO::BUF_BYTES_MAX / SNBUF / (int64_t)sizeof(TIn) / unit * unit;
+    if (p > (int64_t)SGEO::MAXC * SGEO::CHUNK) p = (int64_t)SGEO::MAXC * SGEO::CHUNK / unit * unit;
+    return p < unit ? unit : p;
+}
+
+template <typename TIn, typename TOut>
+int stream_grid() {
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 0;
+    if (!per_sm[dev]) {
+        const int smem = SGEO::smem(stream_portion<TIn, TOut>());
+        cudaFuncSetAttribute(SKERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, SKERN, SGEO::THREADS, smem);
+        per_sm[dev] = b > 0 ? b : -1;
+    }
+    return per_sm[dev] > 0 ? per_sm[dev] * device_sms() : 0;
+}
+
+template <typename TIn, typename TOut>
+int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclusive, uint64_t seed_bits,
+                  const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
+                  uint32_t epoch, cudaStream_t s) {
+    const int64_t G = stream_grid<TIn, TOut>();
+    if (G <= 0 || G > 256) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
+    const int64_t P = stream_portion<TIn, TOut>();
+    const int64_t rounds = (lead + n + P * G - 1) / (P * G);
+    if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
+    StreamArgs a{};
+    a.in = static_cast<const TIn *>(in) - lead;
+    a.out = static_cast<TOut *>(out) - lead;
+    a.lo = lead;
+    a.hi = lead + n;
+    a.portion = P;
+    a.rounds = rounds;
+    a.seed_bits = seed_bits;
+    a.seed_terms = seed_terms;
+    a.n_seed_terms = n_seed_terms;
+    a.total = total;
+    a.desc = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
+    a.epoch = epoch;
+    a.exclusive = exclusive;
+    void *params[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)SKERN, dim3((unsigned)G), dim3(SGEO::THREADS), params,
+                                                SGEO::smem(P), s);
+    return cuda_rc(e);
+}
+
 // ---- scan (1-D and batched share one kernel) ----------------------------------------------
 template <typename TIn, typename TOut>
 int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
@@ -219,6 +287,9 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     if (vec && lead * (int64_t)sizeof(TOut) >= 32) vec = false;
     a.vec_ok = vec;
     a.lead = vec ? lead : 0;
+    if (rows == 1 && vec && g_tune.scan_kernel == 3)
+        return launch_stream<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
+                                        scratch, scratch_bytes, epoch, s);
     if (rows == 1 && vec && g_tune.scan_kernel != 1 &&
         (g_tune.scan_kernel == 2 || cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes))
         return launch_rounds<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
@@ -373,7 +444,10 @@ size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     // the cache-partitioned kernel needs one descriptor per (region, CTA): at most
     // 1024 persistent CTAs, regions of g_tune.round_bytes of input + output
     const int64_t traffic = n * (int64_t)(dsize(dtype_in) + dsize(dtype_out));
-    const int64_t regions = traffic / g_tune.round_bytes + 2 + 2 * g_tune.round_ramp;
+    const int64_t rbytes = g_tune.round_bytes > 0 ? g_tune.round_bytes : (48ll << 20);
+    int64_t regions = traffic / rbytes + 2 + 2 * g_tune.round_ramp;
+    const int64_t stream_regions = n * (int64_t)dsize(dtype_in) / (4ll << 20) + 2;  // >= 4 MiB of input each
+    if (stream_regions > regions) regions = stream_regions;
     const size_t rb = 256 + (size_t)regions * 1024 * 16;
     return bytes > rb ? bytes : rb;
 }
@@ -381,10 +455,10 @@ size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
 int ps_set_tuning(const char *key, int64_t value) {
     if (!key) return PS_ERR_ARG;
     if (!std::strcmp(key, "scan_kernel")) {
-        if (value < 0 || value > 2) return PS_ERR_ARG;
+        if (value < 0 || value > 3) return PS_ERR_ARG;
         g_tune.scan_kernel = (int)value;
     } else if (!std::strcmp(key, "round_bytes")) {
-        if (value < (1ll << 20)) return PS_ERR_ARG;
+        if (value != 0 && value < (1ll << 20)) return PS_ERR_ARG;
         g_tune.round_bytes = value;
     } else if (!std::strcmp(key, "round_lead")) {
         if (value < 1 || value > 8) return PS_ERR_ARG;

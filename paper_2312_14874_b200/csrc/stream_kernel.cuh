@@ -1,0 +1,346 @@
+// stream_kernel.cuh -- shared-memory-resident regions: the partitioned
+// accumulate-scan with each CTA's partition held on chip between its two
+// passes.
+//
+// The reference's cache-partitioned scheme (PAPER.md s2.2, engine.py:278-344)
+// reads every partition twice, relying on the cache to make the second read
+// cheap.  On the B200 the aggregate shared memory of 148 SMs (~30 MB) is the
+// cache we control exactly: a region is sized so that every CTA's portion fits
+// in shared memory several times over, the portion is loaded ONCE from HBM by
+// TMA bulk copies, reduced and scanned from shared memory, and written once --
+// one read and one write per element, no L2 re-read that could miss.
+//
+// Warp roles of one persistent CTA per SM (cooperative launch):
+//   producer warp   TMA bulk copies of region r into buffer r % NBUF once the
+//                   scanners have released it (mbarrier `free`)
+//   RWP reducers    per-chunk totals from shared memory, portion total -> the
+//                   region's global ledger (16-byte epoch-tagged descriptors)
+//   ledger warp     all G portion totals of region r -> per-chunk carries
+//                   (fixed summation order: identical on every CTA)
+//   SW scanners     chunk scans out of shared memory with known carries,
+//                   256-bit streaming stores; release the buffer
+// NBUF buffers let the producer run up to NBUF-1 regions ahead, which hides
+// the grid-wide ledger exchange behind HBM streaming.
+#pragma once
+
+#include "rounds_kernel.cuh"
+
+namespace ps {
+
+struct StreamArgs {
+    const void *in;   // aligned base: position p <-> element p - lead
+    void *out;
+    int64_t lo, hi;   // valid positions
+    int64_t portion;  // positions per CTA per region (multiple of SW * CHUNK)
+    int64_t rounds;   // regions
+    uint64_t seed_bits;
+    const void *seed_terms;
+    int64_t n_seed_terms;
+    void *total;
+    ulonglong2 *desc;  // rounds * G descriptors
+    uint32_t epoch;
+    int exclusive;
+};
+
+template <typename TIn, int SW, int ROWS, int NBUF, int RWP>
+struct StreamGeom {
+    static constexpr int WARPS = SW + RWP + 2;
+    static constexpr int THREADS = WARPS * 32;
+    static constexpr int VEC = 32 / sizeof(TIn);
+    static constexpr int ROW_ELEMS = 32 * VEC;
+    static constexpr int CHUNK = ROWS * ROW_ELEMS;  // one warp's unit (ROWS KiB)
+    static constexpr int MAXC = 64;                 // chunks per portion
+    static constexpr int BUF_BYTES_MAX = 200 * 1024;
+    static constexpr int SMEM_FIXED = 4 * NBUF * 8 + 2 * NBUF * MAXC * 8 + 128;
+    static constexpr int smem(int64_t portion) { return (int)(NBUF * portion * sizeof(TIn)) + SMEM_FIXED; }
+};
+
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP>
+__global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(const StreamArgs a) {
+    using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
+    using A = typename AccOf<TIn>::type;
+    constexpr int VEC = Geo::VEC, ROW_ELEMS = Geo::ROW_ELEMS, CHUNK = Geo::CHUNK, MAXC = Geo::MAXC;
+    constexpr bool FLOAT = (A)0.5 != (A)0;
+    constexpr int RT = RWP * 32;
+    constexpr int BAR_RED = 1;
+    constexpr int W_PROD = SW + RWP, W_LEDGER = SW + RWP + 1;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TIn *buf = reinterpret_cast<TIn *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)NBUF * a.portion * sizeof(TIn));
+    uint64_t *full = bars;             // TMA landed            (1 arrival + tx)
+    uint64_t *red = bars + NBUF;       // chunk totals written  (1)
+    uint64_t *pre = bars + 2 * NBUF;   // chunk carries written (1)
+    uint64_t *freeb = bars + 3 * NBUF; // scanners released it  (SW)
+    A *chunk_tot = reinterpret_cast<A *>(bars + 4 * NBUF);
+    A *chunk_pre = chunk_tot + NBUF * MAXC;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const TIn *in = reinterpret_cast<const TIn *>(a.in);
+    TOut *out = reinterpret_cast<TOut *>(a.out);
+    const uint64_t want = (uint64_t)a.epoch << 2;
+    const int64_t P = a.portion;
+    const int64_t nchunk = P / CHUNK;
+
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&red[b], 1);
+            mbar_init(&pre[b], 1);
+            mbar_init(&freeb[b], SW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // phase of buffer slot b = r % NBUF for region r
+    auto par = [&](int64_t r) { return (uint32_t)((r / NBUF) & 1); };
+    auto p0_of = [&](int64_t r) { return r * P * G + (int64_t)c * P; };
+    auto whole = [&](int64_t r) {
+        const int64_t p0 = p0_of(r);
+        return p0 >= a.lo && p0 + P <= a.hi;
+    };
+    auto live = [&](int64_t r) {  // anything valid in this portion?
+        const int64_t p0 = p0_of(r);
+        return p0 + P > a.lo && p0 < a.hi;
+    };
+
+    if (warp == W_PROD) {
+        // ============================ producer ===================================
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
+                if (whole(r)) {
+                    constexpr uint32_t PIECE = 16384;
+                    const uint32_t bytes = (uint32_t)(P * sizeof(TIn));
+                    mbar_expect_tx(&full[b], bytes);
+                    const char *src = reinterpret_cast<const char *>(in + p0_of(r));
+                    char *dst = reinterpret_cast<char *>(buf + (size_t)b * P);
+                    for (uint32_t o = 0; o < bytes; o += PIECE)
+                        bulk_g2s(dst + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, &full[b], pol);
+                } else {
+                    mbar_arrive(&full[b]);  // boundary portion: consumers read global memory
+                }
+            }
+        }
+        return;
+    }
+
+    if (warp >= SW && warp < W_PROD) {
+        // ============================ reducers ===================================
+        const int rw = warp - SW;
+        for (int64_t r = 0; r < a.rounds; ++r) {
+            const int b = (int)(r % NBUF);
+            mbar_wait(&full[b], par(r));
+            A *tot = chunk_tot + b * MAXC;
+            const TIn *sb = buf + (size_t)b * P;
+            const int64_t p0 = p0_of(r);
+            const bool w = whole(r);
+            for (int64_t ch = rw; ch < nchunk; ch += RWP) {
+                A s = (A)0;
+                if (w) {
+                    V256 raw[ROWS];
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr) {
+                        TIn x[VEC];
+                        unpack<TIn>(raw[rr], x);
+                        s += lane_row_sum<TIn, A, VEC>(x);
+                    }
+                } else if (live(r)) {
+                    for (int rr = 0; rr < ROWS; ++rr)
+                        for (int j = 0; j < VEC; ++j) {
+                            const int64_t pos = p0 + ch * CHUNK + rr * ROW_ELEMS + lane * VEC + j;
+                            if (pos >= a.lo && pos < a.hi) s += (A)in[pos];
+                        }
+                }
+                s = warp_sum(s);
+                if (lane == 0) tot[ch] = s;
+            }
+            // reads of this buffer are done (their sums are stored); order them before
+            // any later TMA refill of the buffer (generic -> async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            named_sync(BAR_RED, RT);
+            if (rw == 0) {
+                A t = (A)0;
+                for (int64_t ch = lane; ch < nchunk; ch += 32) t += tot[ch];
+                t = warp_sum(t);
+                if (lane == 0) {
+                    st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
+                    mbar_arrive(&red[b]);
+                }
+            }
+            named_sync(BAR_RED, RT);
+        }
+        return;
+    }
+
+    if (warp == W_LEDGER) {
+        // ============================ ledger =====================================
+        A carry;
+        {
+            A seed = (A)0;
+            if (a.seed_terms) {
+                const A *st = reinterpret_cast<const A *>(a.seed_terms);
+                for (int64_t i = lane; i < a.n_seed_terms; i += 32) seed += st[i];
+            }
+            carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
+        }
+        constexpr int PER = 8;  // G <= 256
+        for (int64_t r = 0; r < a.rounds; ++r) {
+            const int b = (int)(r % NBUF);
+            ulonglong2 d[PER];
+            unsigned pending = 0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int j = lane + 32 * i;
+                if (j < G) {
+                    d[i] = ld_desc(a.desc + r * G + j);
+                    pending |= 1u << i;
+                }
+            }
+            while (true) {
+#pragma unroll
+                for (int i = 0; i < PER; ++i)
+                    if (((pending >> i) & 1) && (d[i].x & ~3ull) == want && (d[i].x & 3ull) != 0) pending &= ~(1u << i);
+                if (!__any_sync(FULL, pending != 0)) break;
+                __nanosleep(20);
+#pragma unroll
+                for (int i = 0; i < PER; ++i)
+                    if ((pending >> i) & 1) d[i] = ld_desc(a.desc + r * G + lane + 32 * i);
+            }
+            A sb = (A)0, sa = (A)0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int j = lane + 32 * i;
+                if (j < G) {
+                    const A v = acc_from_bits<A>(d[i].y);
+                    sa += v;
+                    if (j < c) sb += v;
+                }
+            }
+            sb = warp_sum(sb);
+            sa = warp_sum(sa);
+            mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
+            const A *tot = chunk_tot + b * MAXC;
+            A *pr = chunk_pre + b * MAXC;
+            // nchunk <= 64: two chunks per lane, exclusive scan across the warp
+            const A t0 = lane * 2 < nchunk ? tot[lane * 2] : (A)0;
+            const A t1 = lane * 2 + 1 < nchunk ? tot[lane * 2 + 1] : (A)0;
+            const A own = t0 + t1;
+            A incl = own;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const A y = shfl_up(incl, dd);
+                if (lane >= dd) incl += y;
+            }
+            A ex = shfl_up(incl, 1);
+            if (lane == 0) ex = (A)0;
+            const A base = carry + sb + ex;
+            if (lane * 2 < nchunk) pr[lane * 2] = base;
+            if (lane * 2 + 1 < nchunk) pr[lane * 2 + 1] = base + t0;
+            carry += sa;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pre[b]);
+        }
+        if (c == 0 && lane == 0 && a.total) *reinterpret_cast<A *>(a.total) = carry;
+        return;
+    }
+
+    // ============================== scanners =======================================
+    const uint64_t pol = policy_evict_first();
+    for (int64_t r = 0; r < a.rounds; ++r) {
+        const int b = (int)(r % NBUF);
+        mbar_wait(&pre[b], par(r));
+        const A *pr = chunk_pre + b * MAXC;
+        const TIn *sb = buf + (size_t)b * P;
+        const int64_t p0 = p0_of(r);
+        const bool w = whole(r);
+        if (w || live(r)) {
+            for (int64_t ch = warp; ch < nchunk; ch += SW) {
+                const int64_t t0 = p0 + ch * CHUNK;
+                A v[ROWS][VEC];
+                if (w) {
+                    V256 raw[ROWS];
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr) {
+                        TIn x[VEC];
+                        unpack<TIn>(raw[rr], x);
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) v[rr][j] = (A)x[j];
+                    }
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            const int64_t pos = t0 + rr * ROW_ELEMS + lane * VEC + j;
+                            v[rr][j] = (pos >= a.lo && pos < a.hi) ? (A)in[pos] : (A)0;
+                        }
+                }
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+                    for (int j = 1; j < VEC; ++j) v[rr][j] += v[rr][j - 1];
+                A sc[ROWS];
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) sc[rr] = v[rr][VEC - 1];
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr) {
+                        const A y = shfl_up(sc[rr], d);
+                        if (lane >= d) sc[rr] += y;
+                    }
+                }
+                A base = pr[ch];
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) {
+                    A ex;
+                    if constexpr (FLOAT) {
+                        ex = shfl_up(sc[rr], 1);
+                        if (lane == 0) ex = (A)0;
+                    } else {
+                        ex = sc[rr] - v[rr][VEC - 1];
+                    }
+                    const A bb = base + ex;
+                    base += shfl_idx(sc[rr], 31);
+                    TOut y[VEC];
+                    if (a.exclusive) {
+                        y[0] = (TOut)bb;
+#pragma unroll
+                        for (int j = 1; j < VEC; ++j) y[j] = (TOut)(bb + v[rr][j - 1]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) y[j] = (TOut)(bb + v[rr][j]);
+                    }
+                    if (w) {
+                        constexpr int NV = VEC * sizeof(TOut) / 32;
+#pragma unroll
+                        for (int q = 0; q < NV; ++q)
+                            stg256_policy(out + t0 + rr * ROW_ELEMS + lane * VEC + q * (32 / sizeof(TOut)),
+                                          pack<TOut>(&y[q * (32 / sizeof(TOut))]), pol);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            const int64_t pos = t0 + rr * ROW_ELEMS + lane * VEC + j;
+                            if (pos >= a.lo && pos < a.hi) out[pos] = y[j];
+                        }
+                    }
+                }
+            }
+        }
+        // every value read from this buffer has been consumed by the stores above
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&freeb[b]);
+    }
+}
+
+}  // namespace ps

@@ -61,8 +61,11 @@ int main(int argc, char **argv) {
         double ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
         double gb = (double)c.n * (c.ei + c.eo) / 1e9;
         printf("%-16s lookback            %8.1f us %7.1f GB/s\n", c.name, ms * 1e3, gb / (ms * 1e-3));
+        PK(ps_set_tuning("scan_kernel", 3));
+        ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
+        printf("%-16s stream (smem regions) %8.1f us %7.1f GB/s\n", c.name, ms * 1e3, gb / (ms * 1e-3));
         PK(ps_set_tuning("scan_kernel", 2));
-        for (int pf : {0, 1})
+        for (int pf : {0})
             for (int64_t rb : rbs) {
                 PK(ps_set_tuning("round_bytes", rb));
                 PK(ps_set_tuning("round_prefetch", pf));

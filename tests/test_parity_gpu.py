@@ -235,7 +235,7 @@ def force_kernel():
         lib.ps_set_tuning(k.encode(), v)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 @pytest.mark.parametrize("dt", [np.int64, np.float32, np.uint32, np.int32, np.float64])
 def test_both_scan_kernels(ps, force_kernel, kernel, dt):
     from paper_2312_14874_b200 import device
@@ -261,9 +261,10 @@ def test_both_scan_kernels(ps, force_kernel, kernel, dt):
                     assert int(tv.item()) == int(xs.astype(np.int64).sum()) + 5, ctx
 
 
-def test_rounds_kernel_widening_and_chaining(ps, force_kernel):
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_rounds_kernel_widening_and_chaining(ps, force_kernel, kernel):
     from paper_2312_14874_b200 import device
-    force_kernel(2)
+    force_kernel(kernel)
     flags = np.random.default_rng(2).integers(0, 2, 3_000_017, dtype=np.int32)
     out = torch.empty(flags.shape[0], dtype=torch.int64, device="cuda")
     tot = device.scan(_cuda(flags), out, exclusive=True, seed_terms=torch.tensor([7, 8], device="cuda"))
@@ -276,9 +277,10 @@ def test_rounds_kernel_widening_and_chaining(ps, force_kernel):
     assert np.array_equal(_host(t), np.cumsum(x.astype(np.float64)).astype(np.float32))
 
 
-def test_rounds_kernel_is_deterministic(ps, force_kernel):
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_rounds_kernel_is_deterministic(ps, force_kernel, kernel):
     from paper_2312_14874_b200 import device
-    force_kernel(2)
+    force_kernel(kernel)
     x = _cuda(np.random.default_rng(4).standard_normal(4_000_037).astype(np.float32))
     outs = []
     for _ in range(3):
@@ -288,12 +290,12 @@ def test_rounds_kernel_is_deterministic(ps, force_kernel):
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
-@pytest.mark.parametrize("round_bytes", [16 << 20, 48 << 20, 96 << 20])
-def test_rounds_kernel_stress_full_size(ps, force_kernel, round_bytes):
+@pytest.mark.parametrize("kernel,round_bytes", [(2, 16 << 20), (2, 48 << 20), (2, 96 << 20), (3, 0)])
+def test_rounds_kernel_stress_full_size(ps, force_kernel, kernel, round_bytes):
     """Many regions x 148 CTAs, repeated: any stage-reuse or ledger race shows up
     as a persistent offset (exact integer comparison over 2^27 elements)."""
     from paper_2312_14874_b200 import device
-    force_kernel(2, round_bytes)
+    force_kernel(kernel, round_bytes or (48 << 20))
     flags = np.random.default_rng(7).integers(0, 2, 1 << 27, dtype=np.int32)
     ref = np.cumsum(flags, dtype=np.int64)
     x = _cuda(flags)
