@@ -446,9 +446,10 @@ size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     const int64_t traffic = n * (int64_t)(dsize(dtype_in) + dsize(dtype_out));
     const int64_t rbytes = g_tune.round_bytes > 0 ? g_tune.round_bytes : (48ll << 20);
     int64_t regions = traffic / rbytes + 2 + 2 * g_tune.round_ramp;
-    const int64_t stream_regions = n * (int64_t)dsize(dtype_in) / (4ll << 20) + 2;  // >= 4 MiB of input each
-    if (stream_regions > regions) regions = stream_regions;
-    const size_t rb = 256 + (size_t)regions * 1024 * 16;
+    size_t rb = 256 + (size_t)regions * 1024 * 16;
+    // stream kernel: <= 256 CTAs, regions of >= 8 MiB of input
+    const size_t sb = 256 + (size_t)(n * (int64_t)dsize(dtype_in) / (8ll << 20) + 2) * 256 * 16;
+    if (sb > rb) rb = sb;
     return bytes > rb ? bytes : rb;
 }
 
