@@ -303,7 +303,7 @@ def run_ours(args, cfg, cfg_name):
     exclusive = cfg["exclusive"]
     scheme = SchemeId(args.scheme)
 
-    if world == 1:
+    if world == 1 and not args.force_sharded:
         def step():
             if rows:
                 device.scan_batched(x, out, exclusive=exclusive)
@@ -354,7 +354,7 @@ def run_ours(args, cfg, cfg_name):
     # dominant kernel: the scan (per-launch CUDA events; at N>1 the step's events
     # also bracket the reduce + all-gather, so use the scan-only loop below)
     kernel_ms = statistics.mean(step_ms)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         kernel_ms = _scan_kernel_ms(device, x, out, exclusive, rows, stream, args.steps)
     esize_in = x.element_size()
     esize_out = out.element_size()
@@ -493,6 +493,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the multi-GPU ShardedScan path even on one GPU (exercises reduce + exchange + carry-in)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

@@ -55,7 +55,7 @@ int main(int argc, char **argv) {
         {"cfg3 i32>i64 ex", 1ll << 28, PS_DTYPE_INT32, PS_DTYPE_INT64, 1, 4, 8},
         {"2^28 i64", 1ll << 28, PS_DTYPE_INT64, PS_DTYPE_INT64, 0, 8, 8},
     };
-    const int64_t rbs[] = {32ll << 20, 40ll << 20, 48ll << 20, 64ll << 20};
+    const int64_t rbs[] = {32ll << 20, 40ll << 20, 48ll << 20, 64ll << 20, 80ll << 20};
     for (const Case &c : cases) {
         PK(ps_set_tuning("scan_kernel", 1));
         double ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
@@ -65,16 +65,16 @@ int main(int argc, char **argv) {
         ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
         printf("%-16s stream (smem regions) %8.1f us %7.1f GB/s\n", c.name, ms * 1e3, gb / (ms * 1e-3));
         PK(ps_set_tuning("scan_kernel", 2));
-        for (int pf : {0})
+        for (int lead : {1, 2})
             for (int64_t rb : rbs) {
                 PK(ps_set_tuning("round_bytes", rb));
-                PK(ps_set_tuning("round_prefetch", pf));
+                PK(ps_set_tuning("round_lead", lead));
                 ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
-                printf("%-16s rounds prefetch=%d R=%3lld MiB %8.1f us %7.1f GB/s\n", c.name, pf, (long long)(rb >> 20),
+                printf("%-16s rounds lead=%d R=%3lld MiB %8.1f us %7.1f GB/s\n", c.name, lead, (long long)(rb >> 20),
                        ms * 1e3, gb / (ms * 1e-3));
             }
-        PK(ps_set_tuning("round_prefetch", 0));
-        PK(ps_set_tuning("round_bytes", 48ll << 20));
+        PK(ps_set_tuning("round_lead", 2));
+        PK(ps_set_tuning("round_bytes", 0));
     }
     return 0;
 }

@@ -57,13 +57,10 @@ int main() {
     CK(cudaMalloc(&in, 1ll << 32)); CK(cudaMalloc(&out, 1ll << 32)); CK(cudaMalloc(&scratch, 64 << 20));
     CK(cudaMemset(in, 0, 1ll << 32)); CK(cudaMemset(scratch, 0, 64 << 20));
     uint32_t epoch = 0;
-    run<float, float, 8, 4, 5, 4, 3>("f32", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 4, 5, 4, 3>("f32_s5r3", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
     run<float, float, 8, 4, 3, 4, 6>("f32_s3r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 8, 4, 4, 4, 5>("f32_s4r5", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<int64_t, int64_t, 8, 4, 5, 4, 3>("cfg1", in, out, 1ll << 24, scratch, epoch, 20ll << 20);
-    run<int64_t, int64_t, 8, 4, 3, 4, 6>("cfg1_s3r6", in, out, 1ll << 24, scratch, epoch, 20ll << 20);
-    run<int64_t, int64_t, 8, 4, 4, 4, 5>("cfg1_s4r5", in, out, 1ll << 24, scratch, epoch, 20ll << 20);
-    run<int64_t, int64_t, 8, 4, 5, 4, 3>("i64", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<int64_t, int64_t, 8, 4, 3, 4, 6>("i64_s3r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 4, 4, 4, 4>("f32_s4r4", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 4, 5, 4, 3>("f32_s5r3_R16", in, out, 1ll << 28, scratch, epoch, 16ll << 20);
+    run<int64_t, int64_t, 8, 4, 5, 4, 3>("i64", in, out, 1ll << 28, scratch, epoch, 32ll << 20);
     return 0;
 }
