@@ -255,6 +255,8 @@ def committed_traffic(config_name):
 def dominant_kernel(lib, cfg, esize_in):
     """Which kernel ps_scan / ps_scan_batched dispatches for this workload."""
     if "rows" in cfg:
+        if lib.ps_get_tuning(b"rows_kernel") != 1 and cfg["rows"] >= 2 * 148:
+            return "scan_rows_kernel (one CTA per row, TMA-streamed 64 KiB segments)"
         return "scan_tiles_kernel (batched rows, decoupled look-back)"
     kern = lib.ps_get_tuning(b"scan_kernel")
     big = cfg["n"] * esize_in >= lib.ps_get_tuning(b"rounds_min_bytes")

@@ -171,6 +171,7 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
  *   "round_lead"       regions the rounds kernel's reducer warps run ahead
  *   "round_ramp"       ramp regions (halving sizes) at each end of the rounds kernel
  *   "round_prefetch"   1 = bulk L2 prefetch of each reducer portion (rounds kernel)
+ *   "rows_kernel"      batched scans: 0 = auto, 1 = look-back tiles, 2 = one CTA per row
  *   "rounds_min_bytes" auto mode uses the rounds kernel from this input size
  * Returns PS_ERR_ARG for an unknown key or value. */
 int ps_set_tuning(const char *key, int64_t value);

@@ -15,6 +15,7 @@
 #include "aux_kernels.cuh"
 #include "rounds_kernel.cuh"
 #include "stream_kernel.cuh"
+#include "rows_kernel.cuh"
 
 namespace ps {
 namespace {
@@ -79,6 +80,7 @@ struct Tuning {
     int64_t round_lead = 2;                 // regions the reducer warps may run ahead of the scanners
     int64_t round_ramp = 0;                 // ramp regions at each end (sizes P/2^k .. P/2); 0 = off
     int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)
+    int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
 };
 Tuning g_tune;
 
@@ -256,6 +258,56 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     cudaError_t e = cudaLaunchCooperativeKernel((const void *)SKERN, dim3((unsigned)G), dim3(SGEO::THREADS), params,
                                                 SGEO::smem(P), s);
     return cuda_rc(e);
+}
+
+// ---- batched rows, one CTA per row (rows_kernel.cuh) ----------------------------------------------
+constexpr int WSW = 8, WRPC = 4, WNBUF = 3, WNCH = 16;
+#define WGEO RowsGeom<TIn, WSW, WRPC, WNBUF, WNCH>
+#define WKERN scan_rows_kernel<TIn, TOut, WSW, WRPC, WNBUF, WNCH>
+
+template <typename TIn, typename TOut>
+int rows_grid() {
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 0;
+    if (!per_sm[dev]) {
+        cudaFuncSetAttribute(WKERN, cudaFuncAttributeMaxDynamicSharedMemorySize, WGEO::SMEM);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, WKERN, WGEO::THREADS, WGEO::SMEM);
+        per_sm[dev] = b > 0 ? b : -1;
+    }
+    return per_sm[dev] > 0 ? per_sm[dev] * device_sms() : 0;
+}
+
+// TMA row streaming needs 16-byte aligned row starts and row lengths
+template <typename TIn, typename TOut>
+bool rows_kernel_applies(const void *in, int64_t rows, int64_t cols, int64_t ld_in) {
+    if (g_tune.rows_kernel == 1) return false;
+    if ((uintptr_t)in % 16 || (cols * (int64_t)sizeof(TIn)) % 16 || (ld_in * (int64_t)sizeof(TIn)) % 16) return false;
+    const int G = rows_grid<TIn, TOut>();
+    if (G <= 0) return false;
+    return g_tune.rows_kernel == 2 || rows >= 2 * (int64_t)G;
+}
+
+template <typename TIn, typename TOut>
+int launch_rows(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int exclusive,
+                const void *row_seeds, void *row_totals, cudaStream_t s) {
+    RowsArgs a{};
+    a.in = in;
+    a.out = out;
+    a.rows = rows;
+    a.cols = cols;
+    a.ld_in = ld_in;
+    a.ld_out = ld_out;
+    a.row_seeds = row_seeds;
+    a.row_totals = row_totals;
+    a.exclusive = exclusive;
+    a.vec_out = (uintptr_t)out % 32 == 0 && (ld_out * (int64_t)sizeof(TOut)) % 32 == 0;
+    int64_t G = rows_grid<TIn, TOut>();
+    if (G > rows) G = rows;
+    WKERN<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+    return launch_rc();
 }
 
 // ---- scan (1-D and batched share one kernel) ----------------------------------------------
@@ -464,6 +516,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "round_lead")) {
         if (value < 1 || value > 8) return PS_ERR_ARG;
         g_tune.round_lead = value;
+    } else if (!std::strcmp(key, "rows_kernel")) {
+        if (value < 0 || value > 2) return PS_ERR_ARG;
+        g_tune.rows_kernel = (int)value;
     } else if (!std::strcmp(key, "round_prefetch")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.round_prefetch = value;
@@ -487,6 +542,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "round_lead")) return g_tune.round_lead;
     if (!std::strcmp(key, "round_ramp")) return g_tune.round_ramp;
     if (!std::strcmp(key, "round_prefetch")) return g_tune.round_prefetch;
+    if (!std::strcmp(key, "rows_kernel")) return g_tune.rows_kernel;
     return -1;
 }
 
@@ -527,6 +583,8 @@ int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64
     if (in == out && (dsize(dtype_in) != dsize(dtype_out) || ld_in != ld_out)) return PS_ERR_OVERLAP;
     if (rows == 1) ld_in = ld_out = cols;
 #define CALL(TI, TO)                                                                                            \
+    if (rows > 1 && rows_kernel_applies<TI, TO>(in, rows, cols, ld_in))                                         \
+        return launch_rows<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, row_seeds, row_totals, s);   \
     return launch_scan<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, 0, row_seeds, row_seeds ? rows : 0, \
                                row_totals, scratch, scratch_bytes, epoch, s)
     PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);

@@ -1,0 +1,226 @@
+// rows_kernel.cuh -- many independent rows (batched scans, cfg4 "delta
+// decoding"): every row is owned by one persistent CTA, so no carry ever
+// crosses a CTA and nothing is exchanged through global memory.
+//
+// Reference semantics: the per-chunk scans of the vertical family
+// (simd.py:164-206: chunk i scanned independently, seeded with a row seed,
+// its running total written out) generalised to `rows` chunks of `cols`
+// elements with a row stride.
+//
+// Per CTA: a producer warp streams (row, segment) work items into a ring of
+// NBUF shared-memory buffers with TMA bulk copies; SW scanner warps first
+// reduce the segment's chunks (4 KiB each) to totals, exchange them through
+// shared memory (one named barrier), then scan their chunks with the carry
+// (row seed + earlier segments + earlier chunks) and store with 256-bit
+// streaming stores.  Each element is read from HBM once and written once.
+#pragma once
+
+#include "stream_kernel.cuh"
+
+namespace ps {
+
+struct RowsArgs {
+    const void *in;
+    void *out;
+    int64_t rows, cols, ld_in, ld_out;  // elements
+    const void *row_seeds;              // acc-typed, nullable
+    void *row_totals;                   // acc-typed, nullable
+    int exclusive;
+    int vec_out;                        // output rows are 32-byte aligned
+};
+
+template <typename TIn, int SW, int RPC, int NBUF, int NCH>
+struct RowsGeom {
+    static constexpr int THREADS = (SW + 1) * 32;
+    static constexpr int VEC = 32 / sizeof(TIn);
+    static constexpr int ROW_ELEMS = 32 * VEC;
+    static constexpr int CHUNK = RPC * ROW_ELEMS;  // elements per chunk (RPC KiB)
+    static constexpr int SEG = NCH * CHUNK;        // elements per work item
+    static constexpr int SEG_BYTES = SEG * (int)sizeof(TIn);
+    static constexpr int SMEM = NBUF * SEG_BYTES + 2 * NBUF * 8 + NBUF * NCH * 8 + 64;
+};
+
+template <typename TIn, typename TOut, int SW, int RPC, int NBUF, int NCH>
+__global__ void __launch_bounds__((SW + 1) * 32, 1) scan_rows_kernel(const RowsArgs a) {
+    using Geo = RowsGeom<TIn, SW, RPC, NBUF, NCH>;
+    using A = typename AccOf<TIn>::type;
+    constexpr int VEC = Geo::VEC, ROW_ELEMS = Geo::ROW_ELEMS, CHUNK = Geo::CHUNK, SEG = Geo::SEG;
+    constexpr bool FLOAT = (A)0.5 != (A)0;
+    constexpr int BAR_SCAN = 1;
+    static_assert(NCH <= 32, "chunk totals are scanned by one warp");
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TIn *buf = reinterpret_cast<TIn *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)NBUF * Geo::SEG_BYTES);
+    uint64_t *freeb = full + NBUF;
+    A *tot = reinterpret_cast<A *>(freeb + NBUF);  // [NBUF][NCH]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    const TIn *in = reinterpret_cast<const TIn *>(a.in);
+    TOut *out = reinterpret_cast<TOut *>(a.out);
+    const int64_t nseg = (a.cols + SEG - 1) / SEG;
+
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&freeb[b], SW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == SW) {
+        // =========================== producer ======================================
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int64_t item = 0;
+            for (int64_t r = c; r < a.rows; r += G) {
+                for (int64_t sg = 0; sg < nseg; ++sg, ++item) {
+                    const int b = (int)(item % NBUF);
+                    if (item >= NBUF) mbar_wait(&freeb[b], (uint32_t)(((item / NBUF) - 1) & 1));
+                    const int64_t e0 = sg * SEG;
+                    const int64_t cnt = (a.cols - e0) < SEG ? (a.cols - e0) : SEG;
+                    const uint32_t bytes = (uint32_t)(cnt * sizeof(TIn));
+                    mbar_expect_tx(&full[b], bytes);
+                    const char *src = reinterpret_cast<const char *>(in + r * a.ld_in + e0);
+                    char *dst = reinterpret_cast<char *>(buf + (size_t)b * SEG);
+                    for (uint32_t o = 0; o < bytes; o += 16384)
+                        bulk_g2s(dst + o, src + o, bytes - o < 16384u ? bytes - o : 16384u, &full[b], pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ============================= scanner warps ===================================
+    const uint64_t pol = policy_evict_first();
+    const A *seeds = reinterpret_cast<const A *>(a.row_seeds);
+    A *totals = reinterpret_cast<A *>(a.row_totals);
+    int64_t item = 0;
+    for (int64_t r = c; r < a.rows; r += G) {
+        A carry = seeds ? seeds[r] : (A)0;
+        for (int64_t sg = 0; sg < nseg; ++sg, ++item) {
+            const int b = (int)(item % NBUF);
+            mbar_wait(&full[b], (uint32_t)((item / NBUF) & 1));
+            const TIn *sb = buf + (size_t)b * SEG;
+            A *tb = tot + b * NCH;
+            const int64_t e0 = sg * SEG;
+            const int64_t cnt = (a.cols - e0) < SEG ? (a.cols - e0) : SEG;
+            // ---- pass 1 over shared memory: chunk totals ----
+            for (int ch = warp; ch < NCH; ch += SW) {
+                A s = (A)0;
+                if ((int64_t)(ch + 1) * CHUNK <= cnt) {
+#pragma unroll
+                    for (int rr = 0; rr < RPC; ++rr) {
+                        TIn x[VEC];
+                        unpack<TIn>(lds256(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC), x);
+                        s += lane_row_sum<TIn, A, VEC>(x);
+                    }
+                } else {
+                    for (int rr = 0; rr < RPC; ++rr)
+                        for (int j = 0; j < VEC; ++j) {
+                            const int64_t k = (int64_t)ch * CHUNK + rr * ROW_ELEMS + lane * VEC + j;
+                            if (k < cnt) s += (A)sb[k];
+                        }
+                }
+                s = warp_sum(s);
+                if (lane == 0) tb[ch] = s;
+            }
+            named_sync(BAR_SCAN, SW * 32);
+            // ---- chunk carries: exclusive scan of the NCH totals (every warp, same order) ----
+            const A t = lane < NCH ? tb[lane] : (A)0;
+            A inc = t;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const A y = shfl_up(inc, d);
+                if (lane >= d) inc += y;
+            }
+            A exs = shfl_up(inc, 1);
+            if (lane == 0) exs = (A)0;
+            const A seg_total = shfl_idx(inc, 31);
+            // ---- pass 2: scan each chunk from its carry, store ----
+            for (int ch = warp; ch < NCH; ch += SW) {
+                const int64_t k0 = (int64_t)ch * CHUNK;
+                if (k0 >= cnt) break;
+                const bool fullc = k0 + CHUNK <= cnt;
+                A v[RPC][VEC];
+                if (fullc) {
+#pragma unroll
+                    for (int rr = 0; rr < RPC; ++rr) {
+                        TIn x[VEC];
+                        unpack<TIn>(lds256(sb + k0 + rr * ROW_ELEMS + lane * VEC), x);
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) v[rr][j] = (A)x[j];
+                    }
+                } else {
+#pragma unroll
+                    for (int rr = 0; rr < RPC; ++rr)
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            const int64_t k = k0 + rr * ROW_ELEMS + lane * VEC + j;
+                            v[rr][j] = k < cnt ? (A)sb[k] : (A)0;
+                        }
+                }
+#pragma unroll
+                for (int rr = 0; rr < RPC; ++rr)
+#pragma unroll
+                    for (int j = 1; j < VEC; ++j) v[rr][j] += v[rr][j - 1];
+                A sc[RPC];
+#pragma unroll
+                for (int rr = 0; rr < RPC; ++rr) sc[rr] = v[rr][VEC - 1];
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+                    for (int rr = 0; rr < RPC; ++rr) {
+                        const A y = shfl_up(sc[rr], d);
+                        if (lane >= d) sc[rr] += y;
+                    }
+                }
+                A base = carry + shfl_idx(exs, ch);
+                TOut *orow = out + r * a.ld_out + e0 + k0;
+#pragma unroll
+                for (int rr = 0; rr < RPC; ++rr) {
+                    A ex;
+                    if constexpr (FLOAT) {
+                        ex = shfl_up(sc[rr], 1);
+                        if (lane == 0) ex = (A)0;
+                    } else {
+                        ex = sc[rr] - v[rr][VEC - 1];
+                    }
+                    const A bb = base + ex;
+                    base += shfl_idx(sc[rr], 31);
+                    TOut y[VEC];
+                    if (a.exclusive) {
+                        y[0] = (TOut)bb;
+#pragma unroll
+                        for (int j = 1; j < VEC; ++j) y[j] = (TOut)(bb + v[rr][j - 1]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) y[j] = (TOut)(bb + v[rr][j]);
+                    }
+                    if (fullc && a.vec_out) {
+                        constexpr int NV = VEC * sizeof(TOut) / 32;
+#pragma unroll
+                        for (int q = 0; q < NV; ++q)
+                            stg256_policy(orow + rr * ROW_ELEMS + lane * VEC + q * (32 / sizeof(TOut)),
+                                          pack<TOut>(&y[q * (32 / sizeof(TOut))]), pol);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j)
+                            if (k0 + rr * ROW_ELEMS + lane * VEC + j < cnt) orow[rr * ROW_ELEMS + lane * VEC + j] = y[j];
+                    }
+                }
+            }
+            carry += seg_total;
+            // every value this warp read from buf[b] / tot[b] has been consumed: hand
+            // its share back (the producer waits for all SW warps)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&freeb[b]);
+        }
+        if (totals && warp == 0 && lane == 0) totals[r] = carry;
+    }
+}
+
+}  // namespace ps

@@ -335,11 +335,25 @@ def test_float32_double_accumulation_matches_reference_bitwise(ps):
     assert np.array_equal(_host(t), np.cumsum(x.astype(np.float64)).astype(np.float32))
 
 
-def test_batched_rows_edge_cases(ps):
-    from paper_2312_14874_b200 import device
+@pytest.mark.parametrize("rows_kernel", [1, 2])
+def test_batched_rows_edge_cases(ps, rows_kernel):
+    """Batched rows through both batched kernels (1 = look-back tiles, 2 = one
+    CTA per row streaming 64 KiB TMA segments): single rows, tiny rows, rows
+    spanning several segments, strided rows, unaligned lengths (tiles fallback)."""
+    from paper_2312_14874_b200 import _lib, device
+    lib = _lib.load()
+    saved = lib.ps_get_tuning(b"rows_kernel")
+    lib.ps_set_tuning(b"rows_kernel", rows_kernel)
+    try:
+        _batched_cases(device)
+    finally:
+        lib.ps_set_tuning(b"rows_kernel", saved)
+
+
+def _batched_cases(device):
     r = np.random.default_rng(8)
     for rows, cols, ld in ((1, 1, 1), (3, 5, 8), (7, 8192, 8192), (5, 8193, 8200), (64, 100_000, 100_000),
-                           (2, 0, 4)):
+                           (2, 0, 4), (300, 16384, 16384), (301, 16388, 16400), (1000, 4, 4), (40, 200_000, 200_064)):
         x = r.integers(0, 256, (rows, ld), dtype=np.int32)
         xt = _cuda(x)[:, :cols]
         out = torch.empty((rows, cols), dtype=torch.int64, device="cuda")
@@ -352,6 +366,14 @@ def test_batched_rows_edge_cases(ps):
             if cols:
                 assert np.array_equal(_host(out), exp), (rows, cols, excl)
             assert np.array_equal(_host(tots), inc[:, -1] if cols else np.arange(rows) * 1000)
+    for dt in (np.float32, np.int64, np.uint32):
+        for rows, cols in ((300, 16384), (40, 70_000)):
+            x = GENS[dt](r, rows * cols).reshape(rows, cols)
+            out = torch.empty_like(_cuda(x))
+            tots = torch.empty(rows, dtype=device.acc_dtype(x.dtype), device="cuda")
+            device.scan_batched(_cuda(x), out, row_totals=tots)
+            for i in (0, rows // 2, rows - 1):
+                _assert_array(_host(out[i]), _expected(x[i]), f"{dt.__name__} row {i} {rows}x{cols}")
 
 
 def test_segmented(ps):
