@@ -261,9 +261,12 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
 }
 
 // ---- batched rows, one CTA per row (rows_kernel.cuh) ----------------------------------------------
-constexpr int WSW = 8, WRPC = 4, WNBUF = 3, WNCH = 16;
-#define WGEO RowsGeom<TIn, WSW, WRPC, WNBUF, WNCH>
-#define WKERN scan_rows_kernel<TIn, TOut, WSW, WRPC, WNBUF, WNCH>
+// measured with scripts/rows_variants.cu: float32 rows are compute-heavier and run
+// best as two independent 64 KiB CTAs per SM; integer rows as one 192 KiB CTA
+template <typename TIn> struct RowsCfg { static constexpr int SW = 8, RPC = 4, NBUF = 3, NCH = 16; };
+template <> struct RowsCfg<float> { static constexpr int SW = 8, RPC = 2, NBUF = 2, NCH = 16; };
+#define WGEO RowsGeom<TIn, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH>
+#define WKERN scan_rows_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH>
 
 template <typename TIn, typename TOut>
 int rows_grid() {

@@ -41,7 +41,7 @@ struct RowsGeom {
 };
 
 template <typename TIn, typename TOut, int SW, int RPC, int NBUF, int NCH>
-__global__ void __launch_bounds__((SW + 1) * 32, 1) scan_rows_kernel(const RowsArgs a) {
+__global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_kernel(const RowsArgs a) {
     using Geo = RowsGeom<TIn, SW, RPC, NBUF, NCH>;
     using A = typename AccOf<TIn>::type;
     constexpr int VEC = Geo::VEC, ROW_ELEMS = Geo::ROW_ELEMS, CHUNK = Geo::CHUNK, SEG = Geo::SEG;
