@@ -146,6 +146,52 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// Ledger gather (one warp): waits for the G portion totals of one region and
+// returns the sum of those before CTA c (sb) and of all of them (sa).  Every
+// lane keeps 8 descriptors in flight per polling round, G may be up to 1024;
+// the summation order is the same on every CTA, so `sa` is bit-identical
+// everywhere (float carries stay consistent across CTAs).
+template <typename A>
+__device__ __forceinline__ void gather_totals(const ulonglong2 *desc, int G, int c, uint64_t want, int lane, A &sb,
+                                              A &sa) {
+    constexpr int PER = 8;
+    sb = (A)0;
+    sa = (A)0;
+    for (int g0 = 0; g0 < G; g0 += 32 * PER) {
+        ulonglong2 d[PER];
+        unsigned pending = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int j = g0 + lane + 32 * i;
+            if (j < G) {
+                d[i] = ld_desc(desc + j);
+                pending |= 1u << i;
+            }
+        }
+        while (true) {
+#pragma unroll
+            for (int i = 0; i < PER; ++i)
+                if (((pending >> i) & 1) && (d[i].x & ~3ull) == want && (d[i].x & 3ull) != 0) pending &= ~(1u << i);
+            if (!__any_sync(FULL, pending != 0)) break;
+            __nanosleep(32);
+#pragma unroll
+            for (int i = 0; i < PER; ++i)
+                if ((pending >> i) & 1) d[i] = ld_desc(desc + g0 + lane + 32 * i);
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int j = g0 + lane + 32 * i;
+            if (j < G) {
+                const A v = acc_from_bits<A>(d[i].y);
+                sa += v;
+                if (j < c) sb += v;
+            }
+        }
+    }
+    sb = warp_sum(sb);
+    sa = warp_sum(sa);
+}
+
 // Warp roles of one persistent CTA (one CTA per SM):
 //   SW scanner warps    pass 2: each warp scans its own chunk of every sub-tile
 //                       with a starting carry known in advance -> no CTA barriers
@@ -221,8 +267,8 @@ __device__ __forceinline__ void lane_prefix(A (&v)[VEC]) {  // in-register inclu
         for (int j = VEC - 1; j >= d; --j) v[j] += v[j - d];
 }
 
-template <typename TIn, typename TOut, int SW, int ROWS, int STAGES, int RWP, int RSTAGES>
-__global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(const RoundArgs a) {
+template <typename TIn, typename TOut, int SW, int ROWS, int STAGES, int RWP, int RSTAGES, int MINB = 1>
+__global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(const RoundArgs a) {
     using Geo = RoundGeom<TIn, TOut, SW, ROWS, STAGES, RWP, RSTAGES>;
     using A = typename AccOf<TIn>::type;
     constexpr int VEC = Geo::VEC, ROW_ELEMS = Geo::ROW_ELEMS, CHUNK = Geo::CHUNK, SUB = Geo::SUB;
@@ -441,41 +487,10 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) scan_rounds_kernel(con
             }
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
         }
-        constexpr int PER = 8;  // descriptors per lane held in registers (G <= 256)
         for (int64_t r = 0; r < a.rounds; ++r) {
-            // all loads of a polling round in flight together; re-poll only the stale ones
-            ulonglong2 d[PER];
-            unsigned pending = 0;
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int j = lane + 32 * i;
-                if (j < G) {
-                    d[i] = ld_desc(a.desc + r * G + j);
-                    pending |= 1u << i;
-                }
-            }
-            while (true) {
-#pragma unroll
-                for (int i = 0; i < PER; ++i)
-                    if (((pending >> i) & 1) && (d[i].x & ~3ull) == want && (d[i].x & 3ull) != 0) pending &= ~(1u << i);
-                if (!__any_sync(FULL, pending != 0)) break;
-                __nanosleep(32);
-#pragma unroll
-                for (int i = 0; i < PER; ++i)
-                    if ((pending >> i) & 1) d[i] = ld_desc(a.desc + r * G + lane + 32 * i);
-            }
-            A sb = (A)0, sa = (A)0;
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int j = lane + 32 * i;
-                if (j < G) {
-                    const A v = acc_from_bits<A>(d[i].y);
-                    sa += v;
-                    if (j < c) sb += v;
-                }
-            }
-            sb = warp_sum(sb);
-            sa = warp_sum(sa);
+            A sb, sa;
+            gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
+
 #ifdef PS_TRACE
             if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 2] = gtimer();
 #endif

@@ -190,41 +190,11 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
             }
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
         }
-        constexpr int PER = 8;  // G <= 256
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
-            ulonglong2 d[PER];
-            unsigned pending = 0;
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int j = lane + 32 * i;
-                if (j < G) {
-                    d[i] = ld_desc(a.desc + r * G + j);
-                    pending |= 1u << i;
-                }
-            }
-            while (true) {
-#pragma unroll
-                for (int i = 0; i < PER; ++i)
-                    if (((pending >> i) & 1) && (d[i].x & ~3ull) == want && (d[i].x & 3ull) != 0) pending &= ~(1u << i);
-                if (!__any_sync(FULL, pending != 0)) break;
-                __nanosleep(20);
-#pragma unroll
-                for (int i = 0; i < PER; ++i)
-                    if ((pending >> i) & 1) d[i] = ld_desc(a.desc + r * G + lane + 32 * i);
-            }
-            A sb = (A)0, sa = (A)0;
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int j = lane + 32 * i;
-                if (j < G) {
-                    const A v = acc_from_bits<A>(d[i].y);
-                    sa += v;
-                    if (j < c) sb += v;
-                }
-            }
-            sb = warp_sum(sb);
-            sa = warp_sum(sa);
+            A sb, sa;
+            gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
+
             mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
             const A *tot = chunk_tot + b * MAXC;
             A *pr = chunk_pre + b * MAXC;

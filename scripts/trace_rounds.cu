@@ -9,10 +9,10 @@
 using namespace ps;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 
-template <typename TIn, typename TOut, int SW, int ROWS, int STAGES, int RWP, int RSTAGES>
+template <typename TIn, typename TOut, int SW, int ROWS, int STAGES, int RWP, int RSTAGES, int MINB = 1>
 void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32_t &epoch, int64_t round_bytes) {
     using Geo = RoundGeom<TIn, TOut, SW, ROWS, STAGES, RWP, RSTAGES>;
-    auto kern = scan_rounds_kernel<TIn, TOut, SW, ROWS, STAGES, RWP, RSTAGES>;
+    auto kern = scan_rounds_kernel<TIn, TOut, SW, ROWS, STAGES, RWP, RSTAGES, MINB>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM));
     int per = 0, sms = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, Geo::THREADS, Geo::SMEM));
@@ -57,10 +57,13 @@ int main() {
     CK(cudaMalloc(&in, 1ll << 32)); CK(cudaMalloc(&out, 1ll << 32)); CK(cudaMalloc(&scratch, 64 << 20));
     CK(cudaMemset(in, 0, 1ll << 32)); CK(cudaMemset(scratch, 0, 64 << 20));
     uint32_t epoch = 0;
-    run<float, float, 8, 4, 5, 4, 3>("f32_s5r3", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 8, 4, 3, 4, 6>("f32_s3r6", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 8, 4, 4, 4, 4>("f32_s4r4", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
-    run<float, float, 8, 4, 5, 4, 3>("f32_s5r3_R16", in, out, 1ll << 28, scratch, epoch, 16ll << 20);
-    run<int64_t, int64_t, 8, 4, 5, 4, 3>("i64", in, out, 1ll << 28, scratch, epoch, 32ll << 20);
+    run<float, float, 8, 4, 3, 4, 6>("f32_1cta", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 2, 4, 4, 4, 2>("f32_2cta_8w", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 6, 2, 4, 2, 6, 2>("f32_2cta_6w", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<float, float, 8, 2, 3, 2, 6, 2>("f32_2cta_8w_r2", in, out, 1ll << 28, scratch, epoch, 24ll << 20);
+    run<int64_t, int64_t, 8, 4, 5, 4, 3>("i64_1cta", in, out, 1ll << 28, scratch, epoch, 32ll << 20);
+    run<int64_t, int64_t, 8, 2, 4, 4, 4, 2>("i64_2cta_8w", in, out, 1ll << 28, scratch, epoch, 32ll << 20);
+    run<int, int64_t, 8, 2, 4, 4, 4, 2>("i32_2cta_8w", in, out, 1ll << 28, scratch, epoch, 21ll << 20);
+    run<int, int64_t, 8, 4, 5, 4, 3>("i32_1cta", in, out, 1ll << 28, scratch, epoch, 21ll << 20);
     return 0;
 }
