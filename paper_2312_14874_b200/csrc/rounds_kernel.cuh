@@ -467,7 +467,14 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                 span_of(r, p0, k_lo, k_hi);
                 for (int64_t k = k_lo; k < k_hi; ++k, ++use) {
                     const uint32_t st = use % STAGES;
+#ifdef PS_TRACE
+                    const int64_t tk = ((r * (a.portion / SUB) + k) * (SW + 1) + SW) * 4;
+                    if (g_trace2 && c == 0) g_trace2[tk] = gtimer();
+#endif
                     mbar_wait(&empty[st], ((use / STAGES) & 1) ^ 1);
+#ifdef PS_TRACE
+                    if (g_trace2 && c == 0) g_trace2[tk + 1] = gtimer();
+#endif
                     mbar_expect_tx(&full[st], Geo::SUB_BYTES);
                     bulk_g2s(stage_buf + (size_t)st * SUB, in + p0 + k * SUB, Geo::SUB_BYTES, &full[st], pol_stream);
                 }
@@ -552,9 +559,16 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
             if (sub0 >= a.hi) break;
             const bool tma = k >= k_lo && k < k_hi;
             A v[ROWS][VEC];
+#ifdef PS_TRACE
+            const int64_t tk = ((r * (a.portion / SUB) + k) * (SW + 1) + warp) * 4;
+            if (g_trace2 && c == 0 && lane == 0) g_trace2[tk] = gtimer();
+#endif
             if (tma) {
                 const uint32_t st = use % STAGES;
                 mbar_wait(&full[st], (use / STAGES) & 1);
+#ifdef PS_TRACE
+                if (g_trace2 && c == 0 && lane == 0) g_trace2[tk + 1] = gtimer();
+#endif
                 const TIn *sb = stage_buf + (size_t)st * SUB + (size_t)warp * CHUNK;
                 V256 raw[ROWS];
 #pragma unroll
@@ -637,6 +651,9 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                     }
                 }
             }
+#ifdef PS_TRACE
+            if (g_trace2 && c == 0 && lane == 0) g_trace2[tk + 2] = gtimer();
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_scan[r & 7]);
