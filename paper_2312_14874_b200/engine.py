@@ -142,7 +142,9 @@ class RunStats:
 
 class ScanEngine:
     """One scan at a time per engine (engine.py:149-155); executes requests
-    on the current CUDA device with the single-pass look-back kernel."""
+    on the current CUDA device through ``core.scan_into`` (one launch of the
+    library's 1-D scan: the L2-region accumulate-scan kernel for large
+    inputs, the decoupled look-back kernel otherwise)."""
 
     def __init__(self, threads: int = 1, affinity: str = "none"):
         if threads < 1:
