@@ -56,6 +56,7 @@ extern "C" {
 #define PS_DTYPE_UINT64 4
 #define PS_DTYPE_FLOAT32 5
 #define PS_DTYPE_FLOAT64 6
+#define PS_DTYPE_UINT8 7    /* flags only (ps_select): byte bitmap / bool */
 
 /* multi-GPU schemes, named after plan.py:24-37 SchemeId */
 #define PS_SCHEME_SCAN_INCREMENT 0   /* scan-then-fixup, 4n bytes  (SCAN_INCREMENT_EQUAL)   */
@@ -162,6 +163,27 @@ int64_t ps_scan_host_epochs(int64_t n, int64_t chunk_elems);
 int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, int dtype_out,
                  int exclusive, uint64_t seed_bits, void *total_host, void *workspace,
                  size_t workspace_bytes, int64_t chunk_elems, uint32_t epoch, void *stream);
+
+/* Bytes of scratch for ps_select over n elements. */
+size_t ps_select_scratch_bytes(int64_t n);
+
+/* Stream compaction / stable partition driven by a flag array -- the consumer
+ * of exclusive offsets the paper motivates the prefix sum with (PAPER.md:34:
+ * "determine the new offsets of data items during a partitioning step ... from
+ * a previously constructed bitmap"; the offsets are ps_scan(flags, exclusive=1),
+ * cf. _scan_kernel core.py:86-92 + exclusive_from_inclusive core.py:141-151).
+ *   values       n elements of dtype_values (any 4- or 8-byte PS_DTYPE_*; bits copied)
+ *   flags        n elements of dtype_flags (PS_DTYPE_UINT8 or any 4/8-byte dtype);
+ *                an element is selected when its flag has any nonzero bit
+ *   partition    0: out[0..k) = selected values in order (k = selected count)
+ *                1: additionally out[k..n) = rejected values in order (stable partition)
+ *   out          device, >= k (partition: n) elements; must not overlap values/flags
+ *   count_out    device int64 (nullable) <- k
+ * Three launches on `stream` (per-8192-element tile counts, exclusive scan of
+ * the counts, scatter through shared memory); the scratch holds the counts
+ * only (no look-back descriptors, no epoch). */
+int ps_select(const void *values, const void *flags, int64_t n, int dtype_values, int dtype_flags, int partition,
+              void *out, void *count_out, void *scratch, size_t scratch_bytes, void *stream);
 
 /* Tuning knobs (process-wide; for benchmarks and tests):
  *   "scan_kernel"      0 = auto, 1 = single-pass decoupled look-back,

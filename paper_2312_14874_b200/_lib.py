@@ -13,7 +13,7 @@ import threading
 
 from . import _build
 
-PS_DTYPE = {"int32": 1, "int64": 2, "uint32": 3, "uint64": 4, "float32": 5, "float64": 6}
+PS_DTYPE = {"int32": 1, "int64": 2, "uint32": 3, "uint64": 4, "float32": 5, "float64": 6, "uint8": 7}
 PS_ERR_DTYPE, PS_ERR_ARG, PS_ERR_SCRATCH, PS_ERR_EPOCH, PS_ERR_OVERLAP = 1, 2, 3, 4, 5
 PS_ERR_CUDA_BASE = 1000
 PS_EPOCH_MAX = 0x3FFFFFFF
@@ -45,6 +45,8 @@ SIGNATURES = {
     "ps_set_tuning": (_i32, [ctypes.c_char_p, _i64]),
     "ps_get_tuning": (_i64, [ctypes.c_char_p]),
     "ps_scan_host": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _u64, _vp, _vp, _sz, _i64, _u32, _vp]),
+    "ps_select_scratch_bytes": (_sz, [_i64]),
+    "ps_select": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
 }
 
 _lib = None

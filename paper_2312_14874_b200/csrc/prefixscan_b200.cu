@@ -16,6 +16,7 @@
 #include "rounds_kernel.cuh"
 #include "stream_kernel.cuh"
 #include "rows_kernel.cuh"
+#include "select_kernels.cuh"
 
 namespace ps {
 namespace {
@@ -819,6 +820,78 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
     cudaStreamWaitEvent(comp, P->end_d2h, 0);
     e = cudaStreamSynchronize(comp);
     return cuda_rc(e);
+}
+
+
+// ---- stream compaction / stable partition (select_kernels.cuh) -----------------------------
+size_t ps_select_scratch_bytes(int64_t n) {
+    if (n < 0) return 0;
+    const int64_t ntiles = (n + SEL_TILE - 1) / SEL_TILE;
+    return 256 + (size_t)ntiles * 8;
+}
+
+int ps_select(const void *values, const void *flags, int64_t n, int dtype_values, int dtype_flags, int partition,
+              void *out, void *count_out, void *scratch, size_t scratch_bytes, void *stream) {
+    const size_t vb = dsize(dtype_values);
+    const size_t fb = dtype_flags == PS_DTYPE_UINT8 ? 1 : dsize(dtype_flags);
+    if (!vb || !fb) return PS_ERR_DTYPE;
+    if (n < 0 || (partition != 0 && partition != 1)) return PS_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        if (count_out) return cuda_rc(cudaMemsetAsync(count_out, 0, 8, s));
+        return PS_OK;
+    }
+    if (!values || !flags || !out) return PS_ERR_ARG;
+    const int64_t ntiles = (n + SEL_TILE - 1) / SEL_TILE;
+    if (ntiles > 0x7fffffffLL) return PS_ERR_ARG;
+    // out may hold up to n elements; it must not touch the inputs
+    if (overlaps_partially(values, (size_t)n * vb, out, (size_t)n * vb) || values == out) return PS_ERR_OVERLAP;
+    if (overlaps_partially(flags, (size_t)n * fb, out, (size_t)n * vb) || flags == out) return PS_ERR_OVERLAP;
+    if (!scratch || scratch_bytes < ps_select_scratch_bytes(n)) return PS_ERR_SCRATCH;
+    char *base = static_cast<char *>(scratch);
+    long long *total = count_out ? static_cast<long long *>(count_out) : reinterpret_cast<long long *>(base);
+    long long *counts = reinterpret_cast<long long *>(base + 256);
+    const uintptr_t va = (uintptr_t)values, fa = (uintptr_t)flags;
+    const int vec_ok = (va % 32 == 0) && (fb == 1 ? fa % 8 == 0 : fa % 32 == 0);
+    int64_t grid = ntiles < 148 * 8 ? ntiles : 148 * 8;
+    // 1) per-tile selected counts
+#define COUNT(TF) \
+    select_count_kernel<TF><<<(unsigned)grid, SEL_THREADS, 0, s>>>(static_cast<const TF *>(flags), n, ntiles, vec_ok, counts)
+    if (fb == 1) COUNT(uint8_t);
+    else if (fb == 4) COUNT(uint32_t);
+    else COUNT(uint64_t);
+#undef COUNT
+    int rc = launch_rc();
+    if (rc) return rc;
+    // 2) exclusive offsets of the tiles + the selected total
+    select_offsets_kernel<<<1, SEL_SCAN_THREADS, 0, s>>>(counts, ntiles, total);
+    rc = launch_rc();
+    if (rc) return rc;
+    // 3) scatter through shared memory
+    const size_t smem = (size_t)SEL_TILE * vb;
+#define SCATTER(TV, TF, P)                                                                                    \
+    do {                                                                                                       \
+        auto k = select_scatter_kernel<TV, TF, P>;                                                             \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                       \
+        k<<<(unsigned)ntiles, SEL_THREADS, smem, s>>>(static_cast<const TV *>(values), static_cast<const TF *>(flags), \
+                                                      n, vec_ok, counts, total, static_cast<TV *>(out));       \
+    } while (0)
+#define BY_FLAG(TV, P)                                   \
+    do {                                                 \
+        if (fb == 1) SCATTER(TV, uint8_t, P);            \
+        else if (fb == 4) SCATTER(TV, uint32_t, P);      \
+        else SCATTER(TV, uint64_t, P);                   \
+    } while (0)
+    if (vb == 4) {
+        if (partition) BY_FLAG(uint32_t, true);
+        else BY_FLAG(uint32_t, false);
+    } else {
+        if (partition) BY_FLAG(uint64_t, true);
+        else BY_FLAG(uint64_t, false);
+    }
+#undef BY_FLAG
+#undef SCATTER
+    return launch_rc();
 }
 
 }  // extern "C"

@@ -208,6 +208,44 @@ def shift_right(x: torch.Tensor, out: torch.Tensor | None = None, identity=0,
     return last
 
 
+_FLAG_CODES = {torch.uint8: 7, torch.bool: 7, torch.int8: 7}
+
+
+def select(values: torch.Tensor, flags: torch.Tensor, out: torch.Tensor | None = None, *,
+           partition: bool = False, count: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Stream compaction (``partition=False``): ``out[:k] = values[flags != 0]``
+    in order; stable partition (``partition=True``): additionally
+    ``out[k:] = values[flags == 0]`` in order.  ``flags`` may be bool/uint8 or
+    any 4/8-byte dtype (nonzero bits select).  Returns ``(out, count)`` with
+    ``count`` a 1-element int64 device tensor (k); nothing is synchronised.
+    ``out`` defaults to a new tensor of ``values``' length."""
+    _require_cuda(values, "values")
+    _require_cuda(flags, "flags")
+    _flat(values, "values")
+    _flat(flags, "flags")
+    if flags.numel() != values.numel():
+        raise ValueError("flags must have one entry per value")
+    cv = dtype_code(values.dtype)
+    cf = _FLAG_CODES.get(flags.dtype)
+    if cf is None:
+        cf = dtype_code(flags.dtype)
+    n = values.numel()
+    if out is None:
+        out = torch.empty_like(values)
+    _require_cuda(out, "out")
+    _flat(out, "out")
+    if out.dtype != values.dtype or out.numel() < n:
+        raise ValueError("out must have values' dtype and at least as many elements")
+    if count is None:
+        count = torch.empty(1, dtype=torch.int64, device=values.device)
+    lib = _lib.load()
+    sptr, sbytes, _ = _scratch_for(values.device, lib.ps_select_scratch_bytes(n), 0, "select")
+    rc = lib.ps_select(_ptr(values), _ptr(flags), n, cv, cf, int(bool(partition)), _ptr(out), _ptr(count),
+                       sptr, sbytes, _stream_ptr(values.device))
+    _lib.check(rc, "ps_select")
+    return out, count
+
+
 def _rows_view(x: torch.Tensor, name: str) -> tuple[int, int, int]:
     if x.dim() != 2:
         raise ValueError(f"{name} must be 2-D (rows, cols)")
