@@ -451,6 +451,9 @@ def _e2e(args, cfg, ps, device, torch, dist, world, rank, dev_t, x, out, tdt, sc
     if world == 1 and not rows:
         def step():  # the drop-in: ps_scan_host pipeline, blocking
             ps.core.scan_into(hin, hout, ps.full_span(hin), 0, exclusive=exclusive)
+    elif world == 1:
+        def step():  # per-row scans of host rows: ps_scan_batched_host pipeline, blocking
+            device.scan_batched_host(hin, hout, exclusive=exclusive)
     else:
         from paper_2312_14874_b200.distributed import ShardedScan
         sharded = ShardedScan(scheme=scheme) if world > 1 else None
@@ -480,8 +483,9 @@ def _e2e(args, cfg, ps, device, torch, dist, world, rank, dev_t, x, out, tdt, sc
     return {"value": x.numel() * world * steps / el, "unit": "elements/s",
             "h2d_bytes_per_step": x.numel() * x.element_size() * world,
             "d2h_bytes_per_step": out.numel() * out.element_size() * world,
-            "steps": steps, "api": "paper_2312_14874_b200.core.scan_into (ps_scan_host)" if world == 1 and not rows
-            else "H2D copy + device API + D2H copy"}
+            "steps": steps, "api": ("paper_2312_14874_b200.core.scan_into (ps_scan_host)" if world == 1 and not rows
+                                    else "paper_2312_14874_b200.device.scan_batched_host (ps_scan_batched_host)"
+                                    if world == 1 else "H2D copy + device API + D2H copy")}
 
 
 def main():

@@ -185,6 +185,19 @@ size_t ps_select_scratch_bytes(int64_t n);
 int ps_select(const void *values, const void *flags, int64_t n, int dtype_values, int dtype_flags, int partition,
               void *out, void *count_out, void *scratch, size_t scratch_bytes, void *stream);
 
+/* Device workspace for ps_scan_batched_host with chunk_rows rows of cols. */
+size_t ps_scan_batched_host_workspace_bytes(int64_t chunk_rows, int64_t cols, int dtype_in, int dtype_out);
+
+/* End-to-end batched scan of contiguous HOST rows (rows x cols, pinned for
+ * full speed): chunks of chunk_rows rows go H2D -> ps_scan_batched -> D2H over
+ * three CUDA streams, so both PCIe directions and the scan overlap.  Rows are
+ * independent (no carry between chunks).  Blocks until out_host is written.
+ * Epochs epoch .. epoch + ceil(rows / chunk_rows) - 1 are used.  The per-row
+ * form of the reference's horizontal_scan(out=) (simd.py:134-148) on host data. */
+int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int64_t cols, int dtype_in,
+                         int dtype_out, int exclusive, void *workspace, size_t workspace_bytes, int64_t chunk_rows,
+                         uint32_t epoch, void *stream);
+
 /* Tuning knobs (process-wide; for benchmarks and tests):
  *   "scan_kernel"      0 = auto, 1 = single-pass decoupled look-back,
  *                      2 = cache-partitioned rounds (persistent, L2 regions),

@@ -823,6 +823,81 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
 }
 
 
+// ---- host-buffer pipeline for batched rows (independent rows: no carry between chunks) ----
+namespace ps {
+namespace {
+HostLayout host_layout_rows(int64_t chunk_rows, int64_t cols, int din, int dout) {
+    HostLayout L{};
+    const int64_t chunk = chunk_rows * cols;
+    L.in_slot = align_up((size_t)chunk * dsize(din), 256);
+    L.out_slot = align_up((size_t)chunk * dsize(dout), 256);
+    L.scratch = align_up(ps_scan_batched_scratch_bytes(chunk_rows, cols, din, dout), 256);
+    L.off_in = 0;
+    L.off_out = L.off_in + NSLOT * L.in_slot;
+    L.off_scratch = L.off_out + NSLOT * L.out_slot;
+    L.off_carry = L.off_scratch + L.scratch;
+    L.total = L.off_carry + 256;
+    return L;
+}
+}  // namespace
+}  // namespace ps
+
+size_t ps_scan_batched_host_workspace_bytes(int64_t chunk_rows, int64_t cols, int dtype_in, int dtype_out) {
+    if (!pair_ok(dtype_in, dtype_out) || chunk_rows <= 0 || cols <= 0) return 0;
+    return host_layout_rows(chunk_rows, cols, dtype_in, dtype_out).total;
+}
+
+int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int64_t cols, int dtype_in,
+                         int dtype_out, int exclusive, void *workspace, size_t workspace_bytes, int64_t chunk_rows,
+                         uint32_t epoch, void *stream) {
+    if (!pair_ok(dtype_in, dtype_out)) return PS_ERR_DTYPE;
+    if (rows < 0 || cols < 0 || chunk_rows <= 0 || (rows > 0 && cols > 0 && (!in_host || !out_host)))
+        return PS_ERR_ARG;
+    const int64_t nchunks = ps_scan_host_epochs(rows, chunk_rows);
+    if (epoch == 0 || (uint64_t)epoch + (uint64_t)nchunks - 1 > PS_EPOCH_MAX) return PS_ERR_EPOCH;
+    if (rows == 0 || cols == 0) return PS_OK;
+    const HostLayout L = host_layout_rows(chunk_rows, cols, dtype_in, dtype_out);
+    if (!workspace || workspace_bytes < L.total) return PS_ERR_SCRATCH;
+    cudaStream_t comp = static_cast<cudaStream_t>(stream);
+    char *ws = static_cast<char *>(workspace);
+    void *scratch = ws + L.off_scratch;
+    HostPipe *P = nullptr;
+    int rc = get_pipe(&P);
+    if (rc) return rc;
+    cudaError_t e;
+    if ((e = cudaEventRecord(P->start, comp)) != cudaSuccess) return cuda_rc(e);
+    cudaStreamWaitEvent(P->h2d, P->start, 0);
+    cudaStreamWaitEvent(P->d2h, P->start, 0);
+    const size_t bi = dsize(dtype_in), bo = dsize(dtype_out);
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int slot = (int)(k % NSLOT);
+        const int64_t r0 = k * chunk_rows;
+        const int64_t nr = (rows - r0) < chunk_rows ? (rows - r0) : chunk_rows;
+        const size_t elems = (size_t)(nr * cols);
+        void *din = ws + L.off_in + slot * L.in_slot;
+        void *dout = ws + L.off_out + slot * L.out_slot;
+        if (k >= NSLOT) cudaStreamWaitEvent(P->h2d, P->d2h_done[slot], 0);
+        e = cudaMemcpyAsync(din, static_cast<const char *>(in_host) + (size_t)(r0 * cols) * bi, elems * bi,
+                            cudaMemcpyHostToDevice, P->h2d);
+        if (e != cudaSuccess) return cuda_rc(e);
+        cudaEventRecord(P->h2d_done[slot], P->h2d);
+        cudaStreamWaitEvent(comp, P->h2d_done[slot], 0);
+        rc = ps_scan_batched(din, dout, nr, cols, cols, cols, dtype_in, dtype_out, exclusive, nullptr, nullptr,
+                             scratch, L.scratch, epoch + (uint32_t)k, comp);
+        if (rc) return rc;
+        cudaEventRecord(P->comp_done[slot], comp);
+        cudaStreamWaitEvent(P->d2h, P->comp_done[slot], 0);
+        e = cudaMemcpyAsync(static_cast<char *>(out_host) + (size_t)(r0 * cols) * bo, dout, elems * bo,
+                            cudaMemcpyDeviceToHost, P->d2h);
+        if (e != cudaSuccess) return cuda_rc(e);
+        cudaEventRecord(P->d2h_done[slot], P->d2h);
+    }
+    cudaEventRecord(P->end_d2h, P->d2h);
+    cudaStreamWaitEvent(comp, P->end_d2h, 0);
+    e = cudaStreamSynchronize(comp);
+    return cuda_rc(e);
+}
+
 // ---- stream compaction / stable partition (select_kernels.cuh) -----------------------------
 size_t ps_select_scratch_bytes(int64_t n) {
     if (n < 0) return 0;

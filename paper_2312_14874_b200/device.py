@@ -336,13 +336,32 @@ def wrapped_block_total(x: torch.Tensor, w: int, seed=0) -> torch.Tensor:
 
 
 # ---- host buffers: the end-to-end entry point ---------------------------------------------------
-DEFAULT_CHUNK_BYTES = 32 << 20  # measured best on PCIe Gen5 (scripts/e2e_sweep.py)
+DEFAULT_CHUNK_BYTES = 32 << 20  # measured best on PCIe Gen5 for large inputs (scripts/e2e_sweep.py)
+MIN_CHUNK_BYTES = 4 << 20  # small inputs: >= 8 chunks so fill/drain stays short
 
 
 class _HostWorkspace:
+    """Device workspace of the host pipelines: NSLOT input/output slots plus
+    epoch-tagged look-back scratch.  The scratch sits at an offset that depends
+    on the slot sizes, so a call with a different layout re-zeroes the buffer:
+    old slot data must never be read back as descriptors."""
+
     def __init__(self):
         self.buf = None
         self.epoch = 0
+        self.layout = None
+
+    def take(self, nbytes: int, n_epochs: int, layout, device: torch.device) -> int:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+            self.epoch = 0
+        elif layout != self.layout or self.epoch + n_epochs > _lib.PS_EPOCH_MAX:
+            self.buf.zero_()
+            self.epoch = 0
+        self.layout = layout
+        first = self.epoch + 1
+        self.epoch += n_epochs
+        return first
 
 
 _host_ws: dict[int, _HostWorkspace] = {}
@@ -378,24 +397,61 @@ def scan_host(x, out=None, *, exclusive: bool = False, seed=0, chunk_elems: int 
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else
                        (device if isinstance(device, int) else device.index or 0))
     if chunk_elems is None:
-        chunk_elems = max(DEFAULT_CHUNK_BYTES // max(_ELEM_BYTES[ci], _ELEM_BYTES[co]), 1 << 16)
+        # >= 8 chunks when the input allows it (pipeline fill/drain is one chunk each
+        # way), but never below MIN_CHUNK_BYTES (per-copy overhead) or above the default
+        eb = max(_ELEM_BYTES[ci], _ELEM_BYTES[co])
+        want = min(DEFAULT_CHUNK_BYTES, max(MIN_CHUNK_BYTES, n * eb // 8))
+        chunk_elems = max(want // eb, 1 << 16)
     wsb = lib.ps_scan_host_workspace_bytes(chunk_elems, ci, co)
     nep = lib.ps_scan_host_epochs(n, chunk_elems)
     with torch.cuda.device(dev):
         ws = _host_ws.setdefault(dev.index, _HostWorkspace())
-        if ws.buf is None or ws.buf.numel() < wsb:
-            ws.buf = torch.zeros(wsb, dtype=torch.uint8, device=dev)
-            ws.epoch = 0
-        if ws.epoch + nep > _lib.PS_EPOCH_MAX:
-            ws.buf.zero_()
-            ws.epoch = 0
-        epoch = ws.epoch + 1
-        ws.epoch += nep
+        epoch = ws.take(wsb, nep, ("1d", chunk_elems, ci, co), dev)
         tot = np.zeros(1, np.uint64)
         rc = lib.ps_scan_host(xp, op, n, ci, co, int(bool(exclusive)), acc_bits(seed, ci), tot.ctypes.data,
                               ws.buf.data_ptr(), ws.buf.numel(), chunk_elems, epoch, _stream_ptr(dev))
         _lib.check(rc, "ps_scan_host")
     return acc_to_python(tot.view(np.dtype(_acc_np(ci)))[0], ci)
+
+
+def scan_batched_host(x, out=None, *, exclusive: bool = False, chunk_rows: int | None = None,
+                      device: torch.device | int | None = None) -> None:
+    """Per-row scans of a contiguous 2-D HOST array end to end: chunks of rows
+    go H2D -> batched scan -> D2H, pipelined over three streams (both PCIe
+    directions overlap).  ``out`` defaults to ``x`` (in place).  Blocks."""
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda or x.dim() != 2 or not x.is_contiguous():
+            raise ValueError("x must be a contiguous 2-D host tensor")
+        rows, cols = x.shape
+    else:
+        if not isinstance(x, np.ndarray) or x.ndim != 2 or not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("x must be a C-contiguous 2-D numpy array")
+        rows, cols = x.shape
+    out = x if out is None else out
+    if tuple(out.shape) != (rows, cols):
+        raise ValueError("output buffer must match input shape")
+    xp, _, ci = _host_pointer(x.reshape(-1))
+    op, _, co = _host_pointer(out.reshape(-1))
+    lib = _lib.load()
+    if not lib.ps_pair_supported(ci, co):
+        raise ValueError("unsupported dtype pair")
+    if rows == 0 or cols == 0:
+        return
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       (device if isinstance(device, int) else device.index or 0))
+    if chunk_rows is None:
+        eb = max(_ELEM_BYTES[ci], _ELEM_BYTES[co])
+        want = min(DEFAULT_CHUNK_BYTES, max(MIN_CHUNK_BYTES, rows * cols * eb // 8))
+        chunk_rows = max(1, want // (cols * eb))
+    chunk_rows = min(chunk_rows, rows)
+    wsb = lib.ps_scan_batched_host_workspace_bytes(chunk_rows, cols, ci, co)
+    nep = lib.ps_scan_host_epochs(rows, chunk_rows)
+    with torch.cuda.device(dev):
+        ws = _host_ws.setdefault(dev.index, _HostWorkspace())
+        epoch = ws.take(wsb, nep, ("rows", chunk_rows, cols, ci, co), dev)
+        rc = lib.ps_scan_batched_host(xp, op, rows, cols, ci, co, int(bool(exclusive)), ws.buf.data_ptr(),
+                                      ws.buf.numel(), chunk_rows, epoch, _stream_ptr(dev))
+        _lib.check(rc, "ps_scan_batched_host")
 
 
 def _acc_np(code: int):
