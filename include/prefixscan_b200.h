@@ -208,6 +208,11 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "round_prefetch"   1 = bulk L2 prefetch of each reducer portion (rounds kernel)
  *   "rows_kernel"      batched scans: 0 = auto, 1 = look-back tiles, 2 = one CTA per row
  *   "rounds_min_bytes" auto mode uses the rounds kernel from this input size
+ *   "stall_seed" / "stall_prob" / "stall_ns"
+ *                      stress tests only: every role hand-off of the look-back,
+ *                      rounds and rows kernels sleeps with probability
+ *                      stall_prob/1024 for a hashed time in [0, stall_ns)
+ *                      (stall_ns 0 = off; the reference's delay_hook, engine.py:91)
  * Returns PS_ERR_ARG for an unknown key or value. */
 int ps_set_tuning(const char *key, int64_t value);
 int64_t ps_get_tuning(const char *key); /* -1 for an unknown key */

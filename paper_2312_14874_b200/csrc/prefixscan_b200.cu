@@ -82,6 +82,7 @@ struct Tuning {
     int64_t round_ramp = 0;                 // ramp regions at each end (sizes P/2^k .. P/2); 0 = off
     int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)
     int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
+    Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
 };
 Tuning g_tune;
 
@@ -94,6 +95,7 @@ template <typename TIn> struct RingSplit { static constexpr int RS = 5, RRS = 3;
 template <> struct RingSplit<float> { static constexpr int RS = 3, RRS = 6; };
 #define RGEO RoundGeom<TIn, TOut, RW, RR, RingSplit<TIn>::RS, RRED, RingSplit<TIn>::RRS>
 #define RKERN scan_rounds_kernel<TIn, TOut, RW, RR, RingSplit<TIn>::RS, RRED, RingSplit<TIn>::RRS>
+#define RKERN_STALL scan_rounds_kernel<TIn, TOut, RW, RR, RingSplit<TIn>::RS, RRED, RingSplit<TIn>::RRS, 1, true>
 
 struct DevInfo {
     int sms = 0;
@@ -180,6 +182,7 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
     const int64_t G = pl.G;
     if (!scratch || scratch_bytes < 256 + (size_t)(pl.rounds * G) * 16) return PS_ERR_SCRATCH;
     RoundArgs a{};
+    a.stall = g_tune.stall;
     a.in = static_cast<const TIn *>(in) - lead;
     a.out = static_cast<TOut *>(out) - lead;
     a.lo = lead;
@@ -198,8 +201,12 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
     a.lead_regions = (int)g_tune.round_lead;
     a.l2_prefetch = (int)g_tune.round_prefetch;
     void *params[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)RKERN,
-                                                dim3((unsigned)G), dim3(Geo::THREADS), params, Geo::SMEM, s);
+    const void *kern = (const void *)RKERN;
+    if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
+        kern = (const void *)RKERN_STALL;
+        if (Geo::SMEM > 48 * 1024) cudaFuncSetAttribute(RKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+    }
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(Geo::THREADS), params, Geo::SMEM, s);
     return cuda_rc(e);
 }
 
@@ -268,6 +275,8 @@ template <typename TIn> struct RowsCfg { static constexpr int SW = 8, RPC = 4, N
 template <> struct RowsCfg<float> { static constexpr int SW = 8, RPC = 2, NBUF = 2, NCH = 16; };
 #define WGEO RowsGeom<TIn, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH>
 #define WKERN scan_rows_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH>
+#define WKERN_STALL \
+    scan_rows_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH, true>
 
 template <typename TIn, typename TOut>
 int rows_grid() {
@@ -298,6 +307,7 @@ template <typename TIn, typename TOut>
 int launch_rows(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int exclusive,
                 const void *row_seeds, void *row_totals, cudaStream_t s) {
     RowsArgs a{};
+    a.stall = g_tune.stall;
     a.in = in;
     a.out = out;
     a.rows = rows;
@@ -310,7 +320,12 @@ int launch_rows(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     a.vec_out = (uintptr_t)out % 32 == 0 && (ld_out * (int64_t)sizeof(TOut)) % 32 == 0;
     int64_t G = rows_grid<TIn, TOut>();
     if (G > rows) G = rows;
-    WKERN<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+    if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
+        cudaFuncSetAttribute(WKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, WGEO::SMEM);
+        WKERN_STALL<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+    } else {
+        WKERN<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+    }
     return launch_rc();
 }
 
@@ -321,6 +336,7 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
                 void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s) {
     constexpr int64_t TILE = tile_elems<TIn>();
     ScanArgs a{};
+    a.stall = g_tune.stall;
     a.in = in;
     a.out = out;
     a.rows = rows;
@@ -523,6 +539,15 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "rows_kernel")) {
         if (value < 0 || value > 2) return PS_ERR_ARG;
         g_tune.rows_kernel = (int)value;
+    } else if (!std::strcmp(key, "stall_seed")) {
+        if (value < 0 || value > 0xffffffffLL) return PS_ERR_ARG;
+        g_tune.stall.seed = (uint32_t)value;
+    } else if (!std::strcmp(key, "stall_prob")) {
+        if (value < 0 || value > 1024) return PS_ERR_ARG;
+        g_tune.stall.prob = (uint32_t)value;
+    } else if (!std::strcmp(key, "stall_ns")) {
+        if (value < 0 || value > 10000000) return PS_ERR_ARG;
+        g_tune.stall.max_ns = (uint32_t)value;
     } else if (!std::strcmp(key, "round_prefetch")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.round_prefetch = value;
@@ -547,6 +572,9 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "round_ramp")) return g_tune.round_ramp;
     if (!std::strcmp(key, "round_prefetch")) return g_tune.round_prefetch;
     if (!std::strcmp(key, "rows_kernel")) return g_tune.rows_kernel;
+    if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
+    if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
+    if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;
     return -1;
 }
 

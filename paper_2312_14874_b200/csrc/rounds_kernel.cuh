@@ -91,6 +91,7 @@ __device__ __forceinline__ V256 lds256(const void *p) {
 }
 
 struct RoundArgs {
+    Stall stall;      // stress tests: stall injection at every role hand-off
     const void *in;   // aligned base: position p <-> element p - lead
     void *out;
     int64_t lo, hi;   // valid positions [lo, hi) (lo = lead, hi = lead + n)
@@ -267,7 +268,8 @@ __device__ __forceinline__ void lane_prefix(A (&v)[VEC]) {  // in-register inclu
         for (int j = VEC - 1; j >= d; --j) v[j] += v[j - d];
 }
 
-template <typename TIn, typename TOut, int SW, int ROWS, int STAGES, int RWP, int RSTAGES, int MINB = 1>
+template <typename TIn, typename TOut, int SW, int ROWS, int STAGES, int RWP, int RSTAGES, int MINB = 1,
+          bool STALL = false>
 __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(const RoundArgs a) {
     using Geo = RoundGeom<TIn, TOut, SW, ROWS, STAGES, RWP, RSTAGES>;
     using A = typename AccOf<TIn>::type;
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                 }
                 for (int64_t k = 0; k < nrsub; ++k, ++use) {
                     const uint32_t st = use % RSTAGES;
+                    stall_site<STALL>(a.stall, r * G + c, k, 3);
                     mbar_wait(&rempty[st], ((use / RSTAGES) & 1) ^ 1);
                     mbar_expect_tx(&rfull[st], Geo::RSUB_BYTES);
                     bulk_g2s(rstage_buf + (size_t)st * RSUB, in + p0 + k * RSUB, Geo::RSUB_BYTES, &rfull[st], pol_keep);
@@ -395,6 +398,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
         uint32_t use = 0;
         for (int64_t r = 0; r < a.rounds; ++r) {
             wait_reducer_may_start(r);
+            stall_site<STALL>(a.stall, r * G + c, rw, 1);
 #ifdef PS_TRACE
             if (g_trace && rw == 0 && lane == 0) g_trace[(r * G + c) * 8 + 0] = gtimer();
 #endif
@@ -443,6 +447,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                 A t = (A)0;
                 for (int64_t ch = lane; ch < nchunk; ch += 32) t += tot[ch];
                 t = warp_sum(t);
+                stall_site<STALL>(a.stall, r * G + c, 0, 2);
                 if (lane == 0) {
                     st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
                     __threadfence_block();
@@ -467,6 +472,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                 span_of(r, p0, k_lo, k_hi);
                 for (int64_t k = k_lo; k < k_hi; ++k, ++use) {
                     const uint32_t st = use % STAGES;
+                    stall_site<STALL>(a.stall, r * G + c, k, 8);
 #ifdef PS_TRACE
                     const int64_t tk = ((r * (a.portion / SUB) + k) * (SW + 1) + SW) * 4;
                     if (g_trace2 && c == 0) g_trace2[tk] = gtimer();
@@ -496,6 +502,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
         }
         for (int64_t r = 0; r < a.rounds; ++r) {
             A sb, sa;
+            stall_site<STALL>(a.stall, r * G + c, 0, 4);
             gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
 
 #ifdef PS_TRACE
@@ -528,6 +535,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                 run += tot[ch];
             }
             carry += sa;
+            stall_site<STALL>(a.stall, r * G + c, 0, 5);
             __syncwarp();
             __threadfence_block();
             if (lane == 0) mbar_arrive(&bar_pre[r & 1]);
@@ -544,6 +552,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
     uint32_t use = 0;
     for (int64_t r = 0; r < a.rounds; ++r) {
         wait_prefixed(r);
+        stall_site<STALL>(a.stall, r * G + c, warp, 6);
 #ifdef PS_TRACE
         if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
 #endif
@@ -558,6 +567,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
             if (sub0 + SUB <= a.lo) continue;
             if (sub0 >= a.hi) break;
             const bool tma = k >= k_lo && k < k_hi;
+            stall_site<STALL>(a.stall, (r * G + c) * 4096 + k, warp, 7);
             A v[ROWS][VEC];
 #ifdef PS_TRACE
             const int64_t tk = ((r * (a.portion / SUB) + k) * (SW + 1) + warp) * 4;

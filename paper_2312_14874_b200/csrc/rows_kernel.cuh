@@ -27,6 +27,7 @@ struct RowsArgs {
     void *row_totals;                   // acc-typed, nullable
     int exclusive;
     int vec_out;                        // output rows are 32-byte aligned
+    Stall stall;                        // stress tests: stall injection
 };
 
 template <typename TIn, int SW, int RPC, int NBUF, int NCH>
@@ -40,7 +41,7 @@ struct RowsGeom {
     static constexpr int SMEM = NBUF * SEG_BYTES + 2 * NBUF * 8 + NBUF * NCH * 8 + 64;
 };
 
-template <typename TIn, typename TOut, int SW, int RPC, int NBUF, int NCH>
+template <typename TIn, typename TOut, int SW, int RPC, int NBUF, int NCH, bool STALL = false>
 __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_kernel(const RowsArgs a) {
     using Geo = RowsGeom<TIn, SW, RPC, NBUF, NCH>;
     using A = typename AccOf<TIn>::type;
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
             for (int64_t r = c; r < a.rows; r += G) {
                 for (int64_t sg = 0; sg < nseg; ++sg, ++item) {
                     const int b = (int)(item % NBUF);
+                    stall_site<STALL>(a.stall, r, sg, 1);
                     if (item >= NBUF) mbar_wait(&freeb[b], (uint32_t)(((item / NBUF) - 1) & 1));
                     const int64_t e0 = sg * SEG;
                     const int64_t cnt = (a.cols - e0) < SEG ? (a.cols - e0) : SEG;
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
         A carry = seeds ? seeds[r] : (A)0;
         for (int64_t sg = 0; sg < nseg; ++sg, ++item) {
             const int b = (int)(item % NBUF);
+            stall_site<STALL>(a.stall, r * 4096 + sg, warp, 2);
             mbar_wait(&full[b], (uint32_t)((item / NBUF) & 1));
             const TIn *sb = buf + (size_t)b * SEG;
             A *tb = tot + b * NCH;

@@ -108,6 +108,44 @@ __device__ __forceinline__ void st_desc(ulonglong2 *p, uint64_t word, uint64_t v
                  ::"l"(p), "l"(word), "l"(value) : "memory");
 }
 
+// In-kernel stall injection (stress tests only; max_ns == 0 disables it and the
+// check is one predictable branch per site).  The GPU form of the reference's
+// delay_hook (engine.py:91, test_engine.py "stalls must never corrupt the
+// double-buffered sums"): a role of one CTA sleeps for a pseudo-random time at
+// a hand-off point, chosen by hashing (seed, a, b, site) -- reproducible.
+struct Stall {
+    uint32_t seed;
+    uint32_t prob;    // stall probability per site visit, in 1/1024 units
+    uint32_t max_ns;  // stall length drawn from [0, max_ns)
+    uint32_t pad;
+};
+__device__ __forceinline__ uint64_t stall_mix(uint64_t x) {  // splitmix64 finaliser
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ void maybe_stall(const Stall &s, uint64_t a, uint64_t b, uint32_t site) {
+    if (s.max_ns == 0) return;
+    const uint64_t h = stall_mix(((uint64_t)s.seed << 32) ^ (a * 0x9E3779B97F4A7C15ull) ^
+                                 (b * 0xC2B2AE3D27D4EB4Full) ^ ((uint64_t)site << 56));
+    if ((uint32_t)(h & 1023) >= s.prob) return;
+    uint32_t ns = (uint32_t)((h >> 10) % s.max_ns);
+    while (ns > 0) {
+        const uint32_t d = ns > 500000u ? 500000u : ns;
+        __nanosleep(d);
+        ns -= d;
+    }
+}
+
+// compile-time gate for the persistent kernels: their stress instantiation has
+// the stall sites, the production one has none (not even the branch)
+template <bool ON>
+__device__ __forceinline__ void stall_site(const Stall &s, uint64_t a, uint64_t b, uint32_t site) {
+    if constexpr (ON) maybe_stall(s, a, b, site);
+}
+
 __device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t epoch, uint64_t st, uint64_t bits) {
     st_desc(d.d + tile, ((uint64_t)epoch << 2) | st, bits);
 }

@@ -36,6 +36,7 @@ struct ScanArgs {
     int exclusive;
     int vec_ok;             // in/out row bases (minus lead) are 32B aligned
     int debug_flags;        // bit 0: skip the look-back (timing experiments only; wrong results)
+    Stall stall;            // stress tests: stall injection at the publication points
 };
 
 template <typename T> __device__ __forceinline__ void unpack(const V256 &v, T (&x)[32 / sizeof(T)]) {
@@ -201,8 +202,10 @@ __global__ void __launch_bounds__(WARPS * 32)
             excl = seed;
             if (lane == 0 && a.tiles_per_row > 1) publish(a.desc, tile, a.epoch, ST_P, acc_to_bits<A>(seed + agg));
         } else {
+            maybe_stall(a.stall, tile, 0, 1);
             if (lane == 0) publish(a.desc, tile, a.epoch, ST_A, acc_to_bits<A>(agg));
             excl = (a.debug_flags & 1) ? (A)0 : lookback<A>(a.desc, tile, head, a.epoch, lane);
+            maybe_stall(a.stall, tile, 0, 2);
             if (lane == 0 && chunk + 1 < a.tiles_per_row)
                 publish(a.desc, tile, a.epoch, ST_P, acc_to_bits<A>(excl + agg));
         }

@@ -208,6 +208,34 @@ def shift_right(x: torch.Tensor, out: torch.Tensor | None = None, identity=0,
     return last
 
 
+class stall_injection:
+    """Context manager: in-kernel stall injection for stress tests (the GPU form
+    of the reference's ``ScanRequest.delay_hook``, engine.py:91).  Every role
+    hand-off of the look-back, rounds and rows kernels sleeps with probability
+    ``prob`` (0..1) for a hashed, reproducible time in [0, ``max_ns``).
+    Process-wide; restores the previous setting on exit."""
+
+    _KEYS = (b"stall_seed", b"stall_prob", b"stall_ns")
+
+    def __init__(self, seed: int = 1, prob: float = 0.1, max_ns: int = 20000):
+        if not 0.0 <= prob <= 1.0 or max_ns < 0 or seed < 0:
+            raise ValueError("stall_injection needs 0 <= prob <= 1, max_ns >= 0, seed >= 0")
+        self.values = (int(seed) & 0xFFFFFFFF, int(round(prob * 1024)), int(max_ns))
+        self.saved = None
+
+    def __enter__(self):
+        lib = _lib.load()
+        self.saved = tuple(lib.ps_get_tuning(k) for k in self._KEYS)
+        for k, v in zip(self._KEYS, self.values):
+            _lib.check(lib.ps_set_tuning(k, v), "ps_set_tuning")
+        return self
+
+    def __exit__(self, *exc):
+        lib = _lib.load()
+        for k, v in zip(self._KEYS, self.saved):
+            lib.ps_set_tuning(k, v)
+
+
 _FLAG_CODES = {torch.uint8: 7, torch.bool: 7, torch.int8: 7}
 
 
