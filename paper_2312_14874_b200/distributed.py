@@ -103,3 +103,122 @@ class ShardedScan:
         if r:
             self.ops.add_offset(out, 0, totals[:r])
         return ShardedScanResult(self.ops.reduce(totals) if want_total else None, totals)
+
+
+class DistributedScanEngine:
+    """Engine-compatible multi-GPU executor (engine.py:131-260 vocabulary).
+
+    ``run(ScanRequest)`` scans this rank's shard (``request.data``, the
+    rank-g piece of a globally contiguous array, EQUAL layout) in the global
+    order and returns the global total as a Python number -- the reference's
+    ``ScanEngine.run`` contract, with the GPUs of the process group in place of
+    the engine's worker threads:
+
+    * ``request.scheme`` is the reference's ``SchemeId``: the EQUAL schemes run
+      as themselves (reduce-then-scan / scan-then-fixup); the PLUS_ONE
+      variants are accepted and run as their EQUAL counterpart (the extra
+      dilated partition balances CPU threads around the idle thread 0;
+      GPU shards are equal by construction);
+    * ``request.delay_hook(rank, 0, "pass1" | "pass2")`` is called on the host
+      before each pass (engine.py:285-314), so delay-injection stress written
+      against the reference drives this engine unchanged;
+    * ``request.collect_stats`` fills ``last_stats`` (``RunStats``): one
+      iteration, one exchange, the per-rank roles of both passes, this rank's
+      kernel launches and HBM bytes (3n/G or 4n/G);
+    * a failure on any rank raises ``RuntimeError`` chained from the cause
+      (engine.py:241-243); ``ValueError`` passes through.
+    """
+
+    _EQUAL = {
+        SchemeId.ACCUMULATE_SCAN_EQUAL: SchemeId.ACCUMULATE_SCAN_EQUAL,
+        SchemeId.ACCUMULATE_SCAN_PLUS_ONE: SchemeId.ACCUMULATE_SCAN_EQUAL,
+        SchemeId.SCAN_INCREMENT_EQUAL: SchemeId.SCAN_INCREMENT_EQUAL,
+        SchemeId.SCAN_INCREMENT_PLUS_ONE: SchemeId.SCAN_INCREMENT_EQUAL,
+    }
+
+    def __init__(self, group=None, ops=None):
+        self.group = group
+        self.ops = ops if ops is not None else CudaOps()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.last_stats = None
+
+    def _all_ok(self, ok: bool) -> bool:
+        """Every rank learns whether any rank failed (the engine's job.failed);
+        all ranks reach this point, failed or not, so nobody blocks in a
+        collective a failed peer never enters (engine.py:313-315)."""
+        if not dist.is_initialized() or self.world == 1:
+            return ok
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64)
+        if dist.get_backend(self.group) == "nccl":
+            flag = flag.cuda()
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(flag.item())
+
+    def run(self, request) -> object:
+        from .engine import RunStats
+        from .plan import Role
+
+        scheme = self._EQUAL.get(request.scheme)
+        if scheme is None:
+            raise ValueError(f"unknown scheme {request.scheme!r}")
+        shard = request.data
+        out = shard if request.out is None else request.out
+        hook = request.delay_hook
+        r, g = self.rank, self.world
+        n = shard.shape[0]
+        ss = ShardedScan(self.group, scheme, self.ops)
+
+        def phase(fn):
+            try:
+                return fn(), None
+            except BaseException as exc:  # noqa: BLE001 - re-raised below, chained
+                return None, exc
+
+        def pass1():
+            if hook is not None:
+                hook(r, 0, "pass1")
+            if scheme is SchemeId.ACCUMULATE_SCAN_EQUAL:
+                return self.ops.reduce(shard)
+            return self.ops.scan(shard, out, exclusive=False, seed=0)
+
+        local, err = phase(pass1)
+        if not self._all_ok(err is None):
+            raise RuntimeError(f"rank {r} failed" if err is not None else "a peer rank failed") from err
+        totals = ss._exchange(local)
+
+        def pass2():
+            if hook is not None:
+                hook(r, 0, "pass2")
+            if scheme is SchemeId.ACCUMULATE_SCAN_EQUAL:
+                self.ops.scan(shard, out, exclusive=False, seed=0, seed_terms=totals[:r] if r else None)
+            elif r:
+                self.ops.add_offset(out, 0, totals[:r])
+            return self.ops.reduce(totals)
+
+        total, err = phase(pass2)
+        if not self._all_ok(err is None):
+            raise RuntimeError(f"rank {r} failed" if err is not None else "a peer rank failed") from err
+        if request.collect_stats:
+            sizes = self._shard_lengths(n)
+            esize = shard.element_size()
+            if scheme is SchemeId.ACCUMULATE_SCAN_EQUAL:
+                p1 = [(t, Role.ACCUMULATE, sizes[t]) for t in range(g)]
+                p2 = [(t, Role.SCAN, sizes[t]) for t in range(g)]
+                launches, nbytes = 3, 3 * n * esize
+            else:
+                p1 = [(t, Role.SCAN, sizes[t]) for t in range(g)]
+                p2 = [(t, Role.INCREMENT, sizes[t]) for t in range(1, g)]
+                launches = 3 if r else 2
+                nbytes = (4 if r else 2) * n * esize
+            self.last_stats = RunStats(iterations=1, barrier_waits=1, sync_points=2, roles=[(p1, p2)],
+                                       kernel_launches=launches, bytes_moved=nbytes)
+        return total.cpu().item()
+
+    def _shard_lengths(self, n_local: int) -> list:
+        """Every rank's shard length (one small all-gather; stats only)."""
+        if not dist.is_initialized() or self.world == 1:
+            return [n_local]
+        parts = [None] * self.world
+        dist.all_gather_object(parts, n_local, group=self.group)
+        return parts

@@ -148,3 +148,118 @@ def test_sharded_scan_rejects_plus_one_schemes():
     from paper_2312_14874_b200.plan import SchemeId
     with pytest.raises(ValueError):
         ShardedScan(scheme=SchemeId.ACCUMULATE_SCAN_PLUS_ONE)
+
+
+# ---- engine-compatible multi-GPU executor (DistributedScanEngine) -----------------------
+
+class FailingOps(OracleOps):
+    """OracleOps whose scan raises on one rank (worker-failure propagation)."""
+
+    def __init__(self, fail_rank):
+        super().__init__()
+        self.fail_rank = fail_rank
+
+    def scan(self, x, out, exclusive=False, seed=0, seed_terms=None):
+        if dist.get_rank() == self.fail_rank:
+            raise OSError("injected device failure")
+        return super().scan(x, out, exclusive, seed, seed_terms)
+
+
+def _engine_worker(rank, world, port, q):
+    import random
+    import time
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_14874_b200.distributed import DistributedScanEngine, shard_span
+        from paper_2312_14874_b200.engine import ScanRequest
+        from paper_2312_14874_b200.plan import Role, SchemeId
+
+        eng = DistributedScanEngine(ops=OracleOps())
+        rng = random.Random(100 + rank)
+        calls = []
+
+        def delay(worker, iteration, phase):
+            calls.append((worker, iteration, phase))
+            if rng.random() < 0.5:
+                time.sleep(rng.random() * 2e-3)
+
+        g = _global_input("int64")
+        sp = shard_span(N, world, rank, 8)
+        res = []
+        for scheme in SchemeId:
+            shard = torch.from_numpy(g[sp.start:sp.end].copy())
+            out = torch.empty_like(shard)
+            total = eng.run(ScanRequest(data=shard, out=out, scheme=scheme, collect_stats=True, delay_hook=delay))
+            st = eng.last_stats
+            p1, p2 = st.roles[0]
+            res.append((scheme.name, sp.start, out.numpy(), int(total), st.iterations, st.kernel_launches,
+                        st.bytes_moved, [(t, role.value, ln) for t, role, ln in p1],
+                        [(t, role.value, ln) for t, role, ln in p2]))
+        # failure on rank 1 -> RuntimeError on every rank, nobody hangs
+        errs = []
+        shard = torch.from_numpy(g[sp.start:sp.end].copy())
+        try:
+            DistributedScanEngine(ops=FailingOps(1)).run(ScanRequest(data=shard, scheme=SchemeId.SCAN_INCREMENT_EQUAL))
+        except RuntimeError as exc:
+            errs.append((str(exc), type(exc.__cause__).__name__ if exc.__cause__ else None))
+        parts = [None] * world
+        dist.all_gather_object(parts, (res, calls, errs))
+        if rank == 0:
+            q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_engine_schemes_stats_hooks_failures(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_engine_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _global_input("int64")
+    want = np.cumsum(g)
+    from paper_2312_14874_b200.plan import SchemeId
+    for si, scheme in enumerate(SchemeId):
+        rows = sorted((parts[r][0][si] for r in range(world)), key=lambda x: x[1])
+        got = np.concatenate([x[2] for x in rows])
+        assert np.array_equal(got, want), scheme
+        assert all(x[3] == int(want[-1]) for x in rows), scheme
+        for rank, x in enumerate(sorted(rows, key=lambda x: x[1])):
+            assert x[4] == 1
+            p1, p2 = x[7], x[8]
+            assert [t for t, _, _ in p1] == list(range(world))
+            assert sum(ln for _, _, ln in p1) == N
+            if "ACCUMULATE" in scheme.name:
+                assert {role for _, role, _ in p1} == {"accumulate"} and {role for _, role, _ in p2} == {"scan"}
+                assert x[6] == 3 * 8 * (x[2].shape[0])
+            else:
+                assert {role for _, role, _ in p2} == {"increment"} and [t for t, _, _ in p2] == list(range(1, world))
+    for r in range(world):
+        calls = parts[r][1]
+        assert calls == [(r, 0, ph) for _ in SchemeId for ph in ("pass1", "pass2")]
+        errs = parts[r][2]
+        assert len(errs) == 1
+        if r == 1:
+            assert errs[0] == ("rank 1 failed", "OSError")
+        else:
+            assert errs[0][0] == "a peer rank failed"
+
+
+def test_distributed_engine_single_process_and_validation():
+    from paper_2312_14874_b200.distributed import DistributedScanEngine
+    from paper_2312_14874_b200.engine import ScanRequest
+    eng = DistributedScanEngine(ops=OracleOps())
+    x = torch.arange(1, 11, dtype=torch.int64)
+    assert eng.run(ScanRequest(data=x)) == 55
+    assert x.tolist() == list(np.cumsum(np.arange(1, 11)))
+    with pytest.raises(ValueError):
+        eng.run(ScanRequest(data=x, scheme="bogus"))
