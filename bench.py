@@ -260,7 +260,9 @@ def dominant_kernel(lib, cfg, esize_in):
         return "scan_tiles_kernel (batched rows, decoupled look-back)"
     kern = lib.ps_get_tuning(b"scan_kernel")
     big = cfg["n"] * esize_in >= lib.ps_get_tuning(b"rounds_min_bytes")
-    if kern == 2 or (kern == 0 and big):
+    if kern == 3 or (kern == 0 and big):
+        return "scan_stream_kernel (accumulate-scan over shared-memory-resident regions)"
+    if kern == 2:
         return "scan_rounds_kernel (cache-partitioned accumulate-scan over L2 regions)"
     return "scan_tiles_kernel (single-pass decoupled look-back)"
 

@@ -211,9 +211,12 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
 }
 
 // ---- shared-memory-resident streaming kernel (stream_kernel.cuh) ---------------------------------
-constexpr int SSW = 8, SROWS = 4, SNBUF = 3, SRWP = 4;
+// measured with scripts/stream_variants.cu: six 32 KiB buffers per SM (regions of
+// 4.6 MiB) hide the grid-wide ledger exchange; three 64 KiB buffers do not
+constexpr int SSW = 8, SROWS = 4, SNBUF = 6, SRWP = 4;
 #define SGEO StreamGeom<TIn, SSW, SROWS, SNBUF, SRWP>
 #define SKERN scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP>
+#define SKERN_STALL scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP, true>
 
 template <typename TIn, typename TOut>
 int64_t stream_portion() {  // positions per CTA per region: NBUF buffers in ~200 KB
@@ -249,6 +252,7 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     const int64_t rounds = (lead + n + P * G - 1) / (P * G);
     if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
     StreamArgs a{};
+    a.stall = g_tune.stall;
     a.in = static_cast<const TIn *>(in) - lead;
     a.out = static_cast<TOut *>(out) - lead;
     a.lo = lead;
@@ -263,8 +267,12 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     a.epoch = epoch;
     a.exclusive = exclusive;
     void *params[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)SKERN, dim3((unsigned)G), dim3(SGEO::THREADS), params,
-                                                SGEO::smem(P), s);
+    const void *kern = (const void *)SKERN;
+    if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
+        kern = (const void *)SKERN_STALL;
+        cudaFuncSetAttribute(SKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, SGEO::smem(P));
+    }
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(SGEO::THREADS), params, SGEO::smem(P), s);
     return cuda_rc(e);
 }
 
@@ -359,11 +367,11 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     if (vec && lead * (int64_t)sizeof(TOut) >= 32) vec = false;
     a.vec_ok = vec;
     a.lead = vec ? lead : 0;
-    if (rows == 1 && vec && g_tune.scan_kernel == 3)
+    const bool big = cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes;
+    if (rows == 1 && vec && (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big)))
         return launch_stream<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
                                         scratch, scratch_bytes, epoch, s);
-    if (rows == 1 && vec && g_tune.scan_kernel != 1 &&
-        (g_tune.scan_kernel == 2 || cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes))
+    if (rows == 1 && vec && g_tune.scan_kernel == 2)
         return launch_rounds<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
                                         scratch, scratch_bytes, epoch, s);
     a.tiles_per_row = (a.lead + cols + TILE - 1) / TILE;
@@ -474,8 +482,7 @@ HostLayout host_layout(int64_t chunk, int din, int dout) {
     HostLayout L{};
     L.in_slot = align_up((size_t)chunk * dsize(din), 256);
     L.out_slot = align_up((size_t)chunk * dsize(dout), 256);
-    const int64_t tiles = (chunk + tile_of_dtype(din) - 1) / tile_of_dtype(din) + 1;
-    L.scratch = align_up(desc_bytes(tiles), 256);
+    L.scratch = align_up(ps_scan_scratch_bytes(chunk, din, dout), 256);  // whichever kernel a chunk takes
     L.off_in = 0;
     L.off_out = L.off_in + NSLOT * L.in_slot;
     L.off_scratch = L.off_out + NSLOT * L.out_slot;
@@ -519,8 +526,8 @@ size_t ps_scan_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     const int64_t rbytes = g_tune.round_bytes > 0 ? g_tune.round_bytes : (48ll << 20);
     int64_t regions = traffic / rbytes + 2 + 2 * g_tune.round_ramp;
     size_t rb = 256 + (size_t)regions * 1024 * 16;
-    // stream kernel: <= 256 CTAs, regions of >= 8 MiB of input
-    const size_t sb = 256 + (size_t)(n * (int64_t)dsize(dtype_in) / (8ll << 20) + 2) * 256 * 16;
+    // stream kernel: <= 256 CTAs, portions of >= 16 KiB of input per CTA and region
+    const size_t sb = 256 + (size_t)(n * (int64_t)dsize(dtype_in) / (16ll << 10) + 2 * 256) * 16;
     if (sb > rb) rb = sb;
     return bytes > rb ? bytes : rb;
 }

@@ -40,6 +40,7 @@ struct StreamArgs {
     ulonglong2 *desc;  // rounds * G descriptors
     uint32_t epoch;
     int exclusive;
+    Stall stall;       // stress tests: stall injection at every role hand-off
 };
 
 template <typename TIn, int SW, int ROWS, int NBUF, int RWP>
@@ -55,7 +56,21 @@ struct StreamGeom {
     static constexpr int smem(int64_t portion) { return (int)(NBUF * portion * sizeof(TIn)) + SMEM_FIXED; }
 };
 
-template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP>
+// widen a warp chunk to the accumulator type.  (A shift-and-rebias float32 ->
+// float64 on the integer pipes, with an F2F fallback for zero/subnormal/inf/nan
+// chunks, measured 16 % slower than F2F here: scripts/stream_variants.cu.)
+template <typename TIn, typename A, int ROWS, int VEC>
+__device__ __forceinline__ void widen_chunk(const V256 (&raw)[ROWS], A (&v)[ROWS][VEC]) {
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr) {
+        TIn x[VEC];
+        unpack<TIn>(raw[rr], x);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[rr][j] = (A)x[j];
+    }
+}
+
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, bool STALL = false>
 __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(const StreamArgs a) {
     using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
     using A = typename AccOf<TIn>::type;
@@ -112,6 +127,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
             const uint64_t pol = policy_evict_first();
             for (int64_t r = 0; r < a.rounds; ++r) {
                 const int b = (int)(r % NBUF);
+                stall_site<STALL>(a.stall, r * G + c, 0, 1);
                 if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
                 if (whole(r)) {
                     constexpr uint32_t PIECE = 16384;
@@ -135,6 +151,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
             mbar_wait(&full[b], par(r));
+            stall_site<STALL>(a.stall, r * G + c, rw, 2);
             A *tot = chunk_tot + b * MAXC;
             const TIn *sb = buf + (size_t)b * P;
             const int64_t p0 = p0_of(r);
@@ -169,6 +186,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
                 A t = (A)0;
                 for (int64_t ch = lane; ch < nchunk; ch += 32) t += tot[ch];
                 t = warp_sum(t);
+                stall_site<STALL>(a.stall, r * G + c, 0, 3);
                 if (lane == 0) {
                     st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
                     mbar_arrive(&red[b]);
@@ -193,6 +211,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
             A sb, sa;
+            stall_site<STALL>(a.stall, r * G + c, 0, 4);
             gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
 
             mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
@@ -214,6 +233,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
             if (lane * 2 < nchunk) pr[lane * 2] = base;
             if (lane * 2 + 1 < nchunk) pr[lane * 2 + 1] = base + t0;
             carry += sa;
+            stall_site<STALL>(a.stall, r * G + c, 0, 5);
             __syncwarp();
             if (lane == 0) mbar_arrive(&pre[b]);
         }
@@ -226,6 +246,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
     for (int64_t r = 0; r < a.rounds; ++r) {
         const int b = (int)(r % NBUF);
         mbar_wait(&pre[b], par(r));
+        stall_site<STALL>(a.stall, r * G + c, warp, 6);
         const A *pr = chunk_pre + b * MAXC;
         const TIn *sb = buf + (size_t)b * P;
         const int64_t p0 = p0_of(r);
@@ -233,18 +254,13 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
         if (w || live(r)) {
             for (int64_t ch = warp; ch < nchunk; ch += SW) {
                 const int64_t t0 = p0 + ch * CHUNK;
+                stall_site<STALL>(a.stall, (r * G + c) * 64 + ch, warp, 7);
                 A v[ROWS][VEC];
                 if (w) {
                     V256 raw[ROWS];
 #pragma unroll
                     for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
-#pragma unroll
-                    for (int rr = 0; rr < ROWS; ++rr) {
-                        TIn x[VEC];
-                        unpack<TIn>(raw[rr], x);
-#pragma unroll
-                        for (int j = 0; j < VEC; ++j) v[rr][j] = (A)x[j];
-                    }
+                    widen_chunk<TIn, A, ROWS, VEC>(raw, v);
                 } else {
 #pragma unroll
                     for (int rr = 0; rr < ROWS; ++rr)

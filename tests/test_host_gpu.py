@@ -76,3 +76,27 @@ def test_host_workspace_layout_changes_stay_correct():
         y = np.empty(x.shape, np.int64)
         dev.scan_batched_host(x, y, chunk_rows=37 + it)
         assert np.array_equal(y, np.cumsum(x, axis=1, dtype=np.int64)), it
+
+
+@pytest.mark.parametrize("n,dt", [(1 << 24, np.int64), ((1 << 24) + 12345, np.float32), (3 << 22, np.int32)])
+def test_host_scan_default_chunks_every_kernel(n, dt):
+    """Default chunk sizes put 16-32 MiB chunks through whichever 1-D kernel the
+    library picks (stream / rounds / tiles): the workspace scratch must fit all."""
+    import contextlib
+    from paper_2312_14874_b200 import _lib, core
+    lib = _lib.load()
+    r = np.random.default_rng(n)
+    a = r.integers(0, 100, n).astype(dt) if np.dtype(dt).kind != "f" else r.random(n, dtype=dt)
+    want = np.cumsum(a.astype(np.float64 if np.dtype(dt).kind == "f" else np.int64))
+    for k in (0, 1, 2, 3):
+        prev = lib.ps_get_tuning(b"scan_kernel")
+        lib.ps_set_tuning(b"scan_kernel", k)
+        try:
+            b = a.copy()
+            core.scan_into(b, None, core.full_span(b), 0)
+        finally:
+            lib.ps_set_tuning(b"scan_kernel", prev)
+        if np.dtype(dt).kind == "f":
+            assert np.max(np.abs(b - want) / np.maximum(want, 1e-30)) <= 1e-6, k
+        else:
+            assert np.array_equal(b, want.astype(dt)), k

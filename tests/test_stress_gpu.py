@@ -41,6 +41,7 @@ KERNELS = {
     "rounds": dict(scan_kernel=2, round_bytes=1 << 20),  # ~1 MiB regions: hundreds of hand-offs
     "rounds_lead1": dict(scan_kernel=2, round_bytes=1 << 20, round_lead=1),
     "tiles": dict(scan_kernel=1),
+    "stream": dict(scan_kernel=3),
 }
 
 
