@@ -199,7 +199,8 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
                          uint32_t epoch, void *stream);
 
 /* Tuning knobs (process-wide; for benchmarks and tests):
- *   "scan_kernel"      0 = auto, 1 = single-pass decoupled look-back,
+ *   "scan_kernel"      0 = auto (3 for large inputs, 1 below rounds_min_bytes),
+ *                      1 = single-pass decoupled look-back,
  *                      2 = cache-partitioned rounds (persistent, L2 regions),
  *                      3 = shared-memory-resident streaming regions (persistent)
  *   "round_bytes"      input + output bytes per L2 region of the rounds kernel (0 = default)
@@ -207,7 +208,8 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "round_ramp"       ramp regions (halving sizes) at each end of the rounds kernel
  *   "round_prefetch"   1 = bulk L2 prefetch of each reducer portion (rounds kernel)
  *   "rows_kernel"      batched scans: 0 = auto, 1 = look-back tiles, 2 = one CTA per row
- *   "rounds_min_bytes" auto mode uses the rounds kernel from this input size
+ *   "rounds_min_bytes" auto mode uses the shared-memory-region (stream) kernel from
+ *                      this input size (smaller inputs: the look-back kernel)
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability
