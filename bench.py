@@ -315,18 +315,23 @@ def run_ours(args, cfg, cfg_name):
                 device.scan(x, out, exclusive=exclusive)
         launches_per_step = 1
     else:
-        sharded = ShardedScan(scheme=scheme)
+        sharded, exchange = _make_sharded(ShardedScan, scheme, args.exchange, world)
 
         def step():
             sharded(x, out, exclusive=exclusive, want_total=False)
-        launches_per_step = 2
+        launches_per_step = 3 if exchange == "p2p" and world > 1 else 2
 
     # ---- verify before timing (bench.py:186-192 convention) ----
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()  # ranks enter the fused exchange together
     step()
     torch.cuda.synchronize()
     parity = None
-    if world == 1 and x_host is not None:
+    if world == 1 and x_host is not None and not args.force_sharded:
         parity = _verify(cfg, x_host, out)
+    elif not rows:
+        parity = _verify_sharded(cfg, x, out, dist, world, rank, torch)
 
     # ---- timed region ----
     for _ in range(args.warmup):
@@ -346,6 +351,9 @@ def run_ours(args, cfg, cfg_name):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    if world > 1 or args.force_sharded:
+        if getattr(sharded, "mailbox", None) is not None:
+            sharded.mailbox.check()  # a fused-exchange wait that gave up invalidates the run
     elapsed_ms = t_start.elapsed_time(t_end)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     if world > 1:
@@ -384,7 +392,8 @@ def run_ours(args, cfg, cfg_name):
             "scaling": "weak", "vs_baseline": None, "dtype": ARITH[cfg["din"]],
             "data": "synthetic (BASELINE.json generator" + (", per-rank shards" if world > 1 else "") + ")",
             "config": {"workload": cfg["desc"], "elements_per_gpu": n,
-                       "parallelism": f"{world} GPU(s), contiguous shards, {scheme.value}" if world > 1 else "1 GPU",
+                       "parallelism": (f"{world} GPU(s), contiguous shards, {scheme.value}, exchange {exchange}"
+                                       if world > 1 or args.force_sharded else "1 GPU"),
                        "l2": "no flush: in+out per step >= 1 GiB >> 126 MB L2"},
             "achieved_gbs": achieved, "hbm_frac_measured": achieved / peak,
             "hbm_frac_nominal": achieved / NOMINAL_HBM_GBS,
@@ -398,6 +407,55 @@ def run_ours(args, cfg, cfg_name):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _make_sharded(ShardedScan, scheme, exchange, world):
+    """The multi-GPU scan with the requested shard-total exchange; the fused
+    peer-memory exchange falls back to the NCCL all-gather (still on the GPU)
+    when the symmetric-memory rendezvous is unavailable on this box."""
+    if exchange == "p2p" and world > 1:
+        try:
+            return ShardedScan(scheme=scheme, exchange="p2p"), "p2p"
+        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+            print(f"bench: fused p2p exchange unavailable ({exc}); using the NCCL all-gather", file=sys.stderr)
+            return ShardedScan(scheme=scheme, exchange="nccl"), f"nccl (p2p unavailable: {type(exc).__name__})"
+    return ShardedScan(scheme=scheme, exchange="nccl"), "nccl" if world > 1 else "none (1 GPU)"
+
+
+def _verify_sharded(cfg, x, out, dist, world, rank, torch):
+    """Size-independent checks of a sharded scan on the device: the first
+    differences of this rank's output reproduce its input, and its first
+    output equals the exact carry (sum of every earlier rank's shard) plus its
+    first input.  Integers exact, float32 within 1e-5 relative."""
+    fl = cfg["din"] == "float32"
+    acc = torch.float64 if fl else torch.int64
+    xs = x.to(acc)
+    o = out.to(acc)
+    local = xs.sum().reshape(1)
+    if world > 1:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local)
+        tot = torch.cat(parts)
+    else:
+        tot = local
+    carry = tot[:rank].sum() if rank else torch.zeros((), dtype=acc, device=x.device)
+    diff_ref = xs[:-1] if cfg["exclusive"] else xs[1:]
+    first = carry if cfg["exclusive"] else carry + xs[0]
+    if fl:
+        scale = torch.maximum(o[-1].abs(), torch.tensor(1e-30, dtype=acc, device=x.device))
+        step_err = float(((o[1:] - o[:-1]) - diff_ref).abs().max() / scale)
+        d_ok = step_err <= 1e-6
+        f_ok = float(((o[0] - first).abs() / torch.clamp(first.abs(), min=1e-30))) <= 1e-5
+    else:
+        d_ok = torch.equal(o[1:] - o[:-1], diff_ref)
+        f_ok = bool((o[0] == first).item())
+    ok = torch.tensor([1 if (d_ok and f_ok) else 0], device=x.device)
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if not int(ok.item()):
+        raise SystemExit("bench: sharded GPU result fails the carry / first-difference checks; refusing to time it")
+    return {"checked": "every rank: first differences reproduce the shard, first output = exact carry "
+                       "(sum of earlier shards) + first input", "ok": True}
 
 
 def _device_input(cfg, g, dev_t, tdt):
@@ -458,7 +516,7 @@ def _e2e(args, cfg, ps, device, torch, dist, world, rank, dev_t, x, out, tdt, sc
             device.scan_batched_host(hin, hout, exclusive=exclusive)
     else:
         from paper_2312_14874_b200.distributed import ShardedScan
-        sharded = ShardedScan(scheme=scheme) if world > 1 else None
+        sharded = _make_sharded(ShardedScan, scheme, args.exchange, world)[0] if world > 1 else None
         dx = torch.empty_like(x)
         dout = torch.empty_like(out)
 
@@ -498,6 +556,9 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--scheme", choices=("accumulate-scan", "scan-increment"), default="accumulate-scan")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1: shard totals through peer-memory mailboxes inside the kernels (p2p, falls back "
+                         "to nccl if unavailable) or one NCCL all-gather between the passes")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -164,6 +164,32 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
                  int exclusive, uint64_t seed_bits, void *total_host, void *workspace,
                  size_t workspace_bytes, int64_t chunk_elems, uint32_t epoch, void *stream);
 
+/* Fused exchange of shard totals over NVLink / NVSwitch (SURVEY.md §8(e) option ii;
+ * replaces the all-gather feeding the ledger fold, engine.py:329-331, across
+ * GPUs).  Every GPU owns a mailbox of 2 x n_peers 16-byte slots (e.g. in
+ * symmetric memory); slot (e & 1) * n_peers + h holds rank h's total of
+ * exchange epoch e.  This call stores {epoch, *total} (device, acc-typed 8
+ * bytes) into that slot of every peer's mailbox -- peer_mailboxes is a DEVICE
+ * array of n_peers mapped base addresses -- with one system-scope 16-byte
+ * store per peer, after waiting (in the kernel) until all n_peers totals of
+ * prev_epoch (0 = none) have arrived in own_mailbox, which guarantees no
+ * slot is overwritten while a slower rank can still read it.  Stream-ordered
+ * after the kernel that produced *total; a wait longer than ~10 s sets
+ * *timeout_flag (device int, nullable) instead of hanging. */
+int ps_publish_total(const void *total, void *const *peer_mailboxes, int n_peers, int rank, uint32_t epoch,
+                     uint32_t prev_epoch, const void *own_mailbox, int *timeout_flag, void *stream);
+
+/* ps_scan whose seed additionally includes the totals found in the n_wait
+ * 16-byte slots at `mailbox` (pass own_mailbox + (e & 1) * n_peers slots: the
+ * ranks before this one) tagged with mail_epoch.  The wait happens inside the scan kernel (the warp that folds
+ * the seed polls; loads and reductions of the first regions proceed), so no
+ * host synchronisation or collective launch sits between the passes.  A wait
+ * longer than ~10 s sets *timeout_flag (device int, nullable) and continues
+ * with zeros instead of hanging. */
+int ps_scan_mailbox(const void *in, void *out, int64_t n, int dtype_in, int dtype_out, int exclusive,
+                    uint64_t seed_bits, const void *mailbox, int n_wait, uint32_t mail_epoch, int *timeout_flag,
+                    void *total_out, void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream);
+
 /* Bytes of scratch for ps_select over n elements. */
 size_t ps_select_scratch_bytes(int64_t n);
 

@@ -175,7 +175,7 @@ bool rounds_plan(int64_t positions, RoundPlan &p) {
 template <typename TIn, typename TOut>
 int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclusive, uint64_t seed_bits,
                   const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
-                  uint32_t epoch, cudaStream_t s) {
+                  uint32_t epoch, cudaStream_t s, const Mailbox *mail = nullptr) {
     using Geo = RGEO;
     RoundPlan pl;
     if (!rounds_plan<TIn, TOut>(lead + n, pl) || pl.G > 1024) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
@@ -183,6 +183,7 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
     if (!scratch || scratch_bytes < 256 + (size_t)(pl.rounds * G) * 16) return PS_ERR_SCRATCH;
     RoundArgs a{};
     a.stall = g_tune.stall;
+    if (mail) a.mail = *mail;
     a.in = static_cast<const TIn *>(in) - lead;
     a.out = static_cast<TOut *>(out) - lead;
     a.lo = lead;
@@ -245,7 +246,7 @@ int stream_grid() {
 template <typename TIn, typename TOut>
 int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclusive, uint64_t seed_bits,
                   const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
-                  uint32_t epoch, cudaStream_t s) {
+                  uint32_t epoch, cudaStream_t s, const Mailbox *mail = nullptr) {
     const int64_t G = stream_grid<TIn, TOut>();
     if (G <= 0 || G > 256) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
     const int64_t P = stream_portion<TIn, TOut>();
@@ -253,6 +254,7 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
     StreamArgs a{};
     a.stall = g_tune.stall;
+    if (mail) a.mail = *mail;
     a.in = static_cast<const TIn *>(in) - lead;
     a.out = static_cast<TOut *>(out) - lead;
     a.lo = lead;
@@ -341,10 +343,12 @@ int launch_rows(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
 template <typename TIn, typename TOut>
 int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
                 int exclusive, uint64_t seed_bits, const void *seed_terms, int64_t n_seed_terms,
-                void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s) {
+                void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s,
+                const Mailbox *mail = nullptr) {
     constexpr int64_t TILE = tile_elems<TIn>();
     ScanArgs a{};
     a.stall = g_tune.stall;
+    if (mail && rows == 1) a.mail = *mail;
     a.in = in;
     a.out = out;
     a.rows = rows;
@@ -370,10 +374,10 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     const bool big = cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes;
     if (rows == 1 && vec && (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big)))
         return launch_stream<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
-                                        scratch, scratch_bytes, epoch, s);
+                                        scratch, scratch_bytes, epoch, s, mail);
     if (rows == 1 && vec && g_tune.scan_kernel == 2)
         return launch_rounds<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
-                                        scratch, scratch_bytes, epoch, s);
+                                        scratch, scratch_bytes, epoch, s, mail);
     a.tiles_per_row = (a.lead + cols + TILE - 1) / TILE;
     const int64_t tiles = rows * a.tiles_per_row;
     if (tiles > 0x7fffffffLL) return PS_ERR_ARG;
@@ -383,6 +387,30 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     }
     scan_tiles_kernel<TIn, TOut, SCAN_WARPS, SCAN_ROWS><<<(unsigned)tiles, SCAN_WARPS * 32, 0, s>>>(a);
     return launch_rc();
+}
+
+// Mailbox layout on every GPU: 2 x n_peers 16-byte slots, slot (e & 1) * n_peers + h
+// holds rank h's total of exchange epoch e.  Before publishing epoch e a rank
+// waits until every rank has published e-1 (prev_epoch): each rank publishes
+// e-1 only after its scan of e-2 has consumed its slots, so a slot of parity
+// e & 1 is never overwritten while a slower rank may still read it.
+__global__ void publish_total_kernel(const uint64_t *total, ulonglong2 *const *peer_mailboxes, int n_peers, int rank,
+                                     uint32_t epoch, uint32_t prev_epoch, const ulonglong2 *own_mailbox,
+                                     int *timeout) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32 && prev_epoch) {
+        Mailbox prev{own_mailbox + (size_t)(prev_epoch & 1) * n_peers, n_peers, prev_epoch, timeout};
+        (void)mailbox_sum<unsigned long long>(prev, lane);
+    }
+    __syncthreads();
+    const int h = threadIdx.x;
+    if (h < n_peers)
+        st_desc_sys(peer_mailboxes[h] + (size_t)(epoch & 1) * n_peers + rank, ((uint64_t)epoch << 2) | ST_A, *total);
+}
+
+template <typename A> __global__ void mailbox_seed_kernel(A *total, uint64_t seed_bits, Mailbox m) {
+    const A v = mailbox_sum<A>(m, threadIdx.x & 31);
+    if (threadIdx.x == 0 && total) *total = acc_from_bits<A>(seed_bits) + v;
 }
 
 template <typename A> __global__ void fill_seed_kernel(A *dst, int64_t count, uint64_t seed_bits, const void *terms,
@@ -931,6 +959,47 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
     cudaStreamWaitEvent(comp, P->end_d2h, 0);
     e = cudaStreamSynchronize(comp);
     return cuda_rc(e);
+}
+
+// ---- fused exchange of shard totals over NVLink (mailboxes) --------------------------------
+int ps_publish_total(const void *total, void *const *peer_mailboxes, int n_peers, int rank, uint32_t epoch,
+                     uint32_t prev_epoch, const void *own_mailbox, int *timeout_flag, void *stream) {
+    if (!total || n_peers < 1 || n_peers > 1024 || rank < 0 || rank >= n_peers || !peer_mailboxes) return PS_ERR_ARG;
+    if (prev_epoch && !own_mailbox) return PS_ERR_ARG;
+    if (epoch == 0 || epoch > PS_EPOCH_MAX || prev_epoch > PS_EPOCH_MAX || (prev_epoch && prev_epoch == epoch))
+        return PS_ERR_EPOCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int threads = ((n_peers + 31) / 32) * 32;
+    publish_total_kernel<<<1, threads, 0, s>>>(static_cast<const uint64_t *>(total),
+                                               reinterpret_cast<ulonglong2 *const *>(peer_mailboxes), n_peers, rank,
+                                               epoch, prev_epoch, static_cast<const ulonglong2 *>(own_mailbox),
+                                               timeout_flag);
+    return launch_rc();
+}
+
+int ps_scan_mailbox(const void *in, void *out, int64_t n, int dtype_in, int dtype_out, int exclusive,
+                    uint64_t seed_bits, const void *mailbox, int n_wait, uint32_t mail_epoch, int *timeout_flag,
+                    void *total_out, void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream) {
+    if (!pair_ok(dtype_in, dtype_out)) return PS_ERR_DTYPE;
+    if (n < 0 || n_wait < 0 || (n > 0 && (!in || !out)) || (n_wait > 0 && !mailbox)) return PS_ERR_ARG;
+    if (epoch == 0 || epoch > PS_EPOCH_MAX || mail_epoch == 0 || mail_epoch > PS_EPOCH_MAX) return PS_ERR_EPOCH;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Mailbox m{static_cast<const ulonglong2 *>(mailbox), n_wait, mail_epoch, timeout_flag};
+    if (n == 0) {
+        if (!total_out) return PS_OK;
+#define SEED(T) mailbox_seed_kernel<typename AccOf<T>::type><<<1, 32, 0, s>>>( \
+        static_cast<typename AccOf<T>::type *>(total_out), seed_bits, m)
+        PS_DISPATCH_ONE(dtype_in, SEED);
+#undef SEED
+        return launch_rc();
+    }
+    if (overlaps_partially(in, (size_t)n * dsize(dtype_in), out, (size_t)n * dsize(dtype_out))) return PS_ERR_OVERLAP;
+    if (in == out && dsize(dtype_in) != dsize(dtype_out)) return PS_ERR_OVERLAP;
+#define CALL(TI, TO)                                                                                          \
+    return launch_scan<TI, TO>(in, out, 1, n, n, n, exclusive, seed_bits, nullptr, 0, total_out, scratch,    \
+                               scratch_bytes, epoch, s, &m)
+    PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);
+#undef CALL
 }
 
 // ---- stream compaction / stable partition (select_kernels.cuh) -----------------------------

@@ -92,6 +92,7 @@ __device__ __forceinline__ V256 lds256(const void *p) {
 
 struct RoundArgs {
     Stall stall;      // stress tests: stall injection at every role hand-off
+    Mailbox mail;     // seed += totals published by the ranks before this one
     const void *in;   // aligned base: position p <-> element p - lead
     void *out;
     int64_t lo, hi;   // valid positions [lo, hi) (lo = lead, hi = lead + n)
@@ -499,6 +500,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, MINB) scan_rounds_kernel(
                 for (int64_t i = lane; i < a.n_seed_terms; i += 32) seed += st[i];
             }
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
+            if (a.mail.n) carry += mailbox_sum<A>(a.mail, lane);
         }
         for (int64_t r = 0; r < a.rounds; ++r) {
             A sb, sa;

@@ -146,6 +146,35 @@ __device__ __forceinline__ void stall_site(const Stall &s, uint64_t a, uint64_t 
     if constexpr (ON) maybe_stall(s, a, b, site);
 }
 
+// ---- cross-GPU mailbox (fused exchange of shard totals over NVLink) ----------------------
+// Rank h's reduce publishes {epoch<<2 | 1, total bits} into slot h of every
+// peer's mailbox with one 16-byte system-scope store (ps_publish_total); a scan
+// that needs the carry of ranks 0..n-1 polls its own mailbox slots 0..n-1
+// from inside the kernel (only the warp that folds the seed waits; loads and
+// reductions of the first regions proceed meanwhile).  A wait that exceeds
+// ~10 s gives up and raises *timeout instead of hanging the GPU.
+struct Mailbox {
+    const ulonglong2 *slots;  // this GPU's mailbox (written by peers)
+    int n;                    // slots to wait for (the ranks before this one)
+    uint32_t epoch;
+    int *timeout;             // device flag, nullable
+};
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ ulonglong2 ld_desc_sys(const ulonglong2 *p) {
+    ulonglong2 v;
+    asm volatile("{ .reg .b128 t; ld.relaxed.sys.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+                 : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_desc_sys(ulonglong2 *p, uint64_t word, uint64_t value) {
+    asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.sys.global.b128 [%0], t; }"
+                 ::"l"(p), "l"(word), "l"(value) : "memory");
+}
+
 __device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t epoch, uint64_t st, uint64_t bits) {
     st_desc(d.d + tile, ((uint64_t)epoch << 2) | st, bits);
 }

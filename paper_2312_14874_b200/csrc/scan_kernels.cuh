@@ -19,6 +19,32 @@
 
 namespace ps {
 
+// Sum of the published totals of mailbox slots 0..m.n-1 (one full warp; the
+// tree order is fixed, so every CTA of a rank folds the same value).
+template <typename A>
+__device__ A mailbox_sum(const Mailbox &m, int lane) {
+    A v = (A)0;
+    const uint64_t want = (uint64_t)m.epoch << 2;
+    for (int j = lane; j < m.n; j += 32) {
+        ulonglong2 d = ld_desc_sys(m.slots + j);
+        if ((d.x & ~3ull) != want || (d.x & 3ull) == 0) {
+            const uint64_t t0 = global_ns();
+            while (true) {
+                __nanosleep(100);
+                d = ld_desc_sys(m.slots + j);
+                if ((d.x & ~3ull) == want && (d.x & 3ull) != 0) break;
+                if (global_ns() - t0 > 10000000000ull) {
+                    if (m.timeout) atomicExch(m.timeout, 1);
+                    d.y = 0;
+                    break;
+                }
+            }
+        }
+        v += acc_from_bits<A>(d.y);
+    }
+    return warp_sum(v);
+}
+
 struct ScanArgs {
     const void *in;
     void *out;
@@ -37,6 +63,7 @@ struct ScanArgs {
     int vec_ok;             // in/out row bases (minus lead) are 32B aligned
     int debug_flags;        // bit 0: skip the look-back (timing experiments only; wrong results)
     Stall stall;            // stress tests: stall injection at the publication points
+    Mailbox mail;           // rows == 1: seed += totals published by the ranks before this one
 };
 
 template <typename T> __device__ __forceinline__ void unpack(const V256 &v, T (&x)[32 / sizeof(T)]) {
@@ -199,6 +226,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                     seed += warp_sum(acc);
                 }
             }
+            if (a.mail.n) seed += mailbox_sum<A>(a.mail, lane);
             excl = seed;
             if (lane == 0 && a.tiles_per_row > 1) publish(a.desc, tile, a.epoch, ST_P, acc_to_bits<A>(seed + agg));
         } else {

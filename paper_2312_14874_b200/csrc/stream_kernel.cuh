@@ -41,6 +41,7 @@ struct StreamArgs {
     uint32_t epoch;
     int exclusive;
     Stall stall;       // stress tests: stall injection at every role hand-off
+    Mailbox mail;      // seed += totals published by the ranks before this one
 };
 
 template <typename TIn, int SW, int ROWS, int NBUF, int RWP>
@@ -70,8 +71,8 @@ __device__ __forceinline__ void widen_chunk(const V256 (&raw)[ROWS], A (&v)[ROWS
     }
 }
 
-template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, bool STALL = false>
-__global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(const StreamArgs a) {
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, bool STALL = false, int MINB = 1>
+__global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(const StreamArgs a) {
     using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
     using A = typename AccOf<TIn>::type;
     constexpr int VEC = Geo::VEC, ROW_ELEMS = Geo::ROW_ELEMS, CHUNK = Geo::CHUNK, MAXC = Geo::MAXC;
@@ -207,12 +208,17 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, 1) scan_stream_kernel(con
                 for (int64_t i = lane; i < a.n_seed_terms; i += 32) seed += st[i];
             }
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
+            if (a.mail.n) carry += mailbox_sum<A>(a.mail, lane);
         }
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
             A sb, sa;
             stall_site<STALL>(a.stall, r * G + c, 0, 4);
+#ifdef PS_EXP_NOLEDGER
+            sb = sa = (A)0;
+#else
             gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
+#endif
 
             mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
             const A *tot = chunk_tot + b * MAXC;

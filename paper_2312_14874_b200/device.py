@@ -208,6 +208,49 @@ def shift_right(x: torch.Tensor, out: torch.Tensor | None = None, identity=0,
     return last
 
 
+def publish_total(total: torch.Tensor, peer_mailboxes: torch.Tensor, rank: int, epoch: int, prev_epoch: int,
+                  own_mailbox: torch.Tensor, timeout: torch.Tensor | None = None) -> None:
+    """Fused shard-total exchange, producer side (ps_publish_total): store
+    ``total`` (1-element accumulator tensor) into this rank's slot of every
+    peer mailbox.  ``peer_mailboxes`` is a device int64 tensor of the peers'
+    mailbox base addresses (2 x G slots of 16 bytes each)."""
+    _require_cuda(total, "total")
+    if peer_mailboxes.dtype != torch.int64 or not peer_mailboxes.is_cuda:
+        raise ValueError("peer_mailboxes must be a CUDA int64 tensor of device addresses")
+    rc = _lib.load().ps_publish_total(_ptr(total), _ptr(peer_mailboxes), peer_mailboxes.numel(), rank, epoch,
+                                      prev_epoch, _ptr(own_mailbox), _ptr(timeout), _stream_ptr(total.device))
+    _lib.check(rc, "ps_publish_total")
+
+
+def scan_mailbox(x: torch.Tensor, out: torch.Tensor | None, mailbox_slots: int, n_wait: int, mail_epoch: int, *,
+                 exclusive: bool = False, seed=0, timeout: torch.Tensor | None = None,
+                 total: torch.Tensor | None = None, dtype=None) -> torch.Tensor:
+    """Fused shard-total exchange, consumer side (ps_scan_mailbox): scan ``x``
+    seeded with ``seed`` plus the totals found in the ``n_wait`` mailbox slots
+    at device address ``mailbox_slots`` under ``mail_epoch``; the wait is inside
+    the scan kernel.  ``x`` may be None (with ``dtype``) to only fold the
+    mailbox into ``total``.  Returns the 1-element accumulator total."""
+    if x is None:
+        code = dtype_code(dtype)
+        dev = total.device if total is not None else torch.device("cuda", torch.cuda.current_device())
+        n, xo, oo, co = 0, None, None, code
+    else:
+        _require_cuda(x, "x")
+        _flat(x, "x")
+        out = x if out is None else out
+        _flat(out, "out")
+        code, co, dev, n, xo, oo = dtype_code(x.dtype), dtype_code(out.dtype), x.device, x.numel(), x, out
+    if total is None:
+        total = torch.empty(1, dtype=_ACC_TORCH[code], device=dev)
+    lib = _lib.load()
+    sptr, sbytes, epoch = _scratch_for(dev, lib.ps_scan_scratch_bytes(max(n, 1), code, co))
+    rc = lib.ps_scan_mailbox(_ptr(xo), _ptr(oo), n, code, co, int(bool(exclusive)), acc_bits(seed, code),
+                             mailbox_slots, n_wait, mail_epoch, _ptr(timeout), _ptr(total), sptr, sbytes, epoch,
+                             _stream_ptr(dev))
+    _lib.check(rc, "ps_scan_mailbox")
+    return total
+
+
 class stall_injection:
     """Context manager: in-kernel stall injection for stress tests (the GPU form
     of the reference's ``ScanRequest.delay_hook``, engine.py:91).  Every role

@@ -65,17 +65,85 @@ class ShardedScanResult:
     shard_totals: torch.Tensor  # the G exchanged shard totals
 
 
-class ShardedScan:
-    """Scan a globally contiguous array whose rank-g piece lives on rank g."""
+class MailboxExchange:
+    """The fused exchange's plumbing: a mailbox of 2 x G 16-byte slots on
+    every GPU and the device array of all G mailbox addresses, so that
+    ``ps_publish_total`` stores straight into the peers' memory over NVLink /
+    NVSwitch and ``ps_scan_mailbox`` polls its own mailbox from inside the
+    scan kernel (SURVEY.md §8(e) option ii) -- no collective launch, no host
+    synchronisation between the passes.
 
-    def __init__(self, group=None, scheme: SchemeId = SchemeId.ACCUMULATE_SCAN_EQUAL, ops=None):
+    ``bases`` are the mailbox base addresses indexed by rank: from a
+    symmetric-memory rendezvous across processes (``from_group``), or any
+    list of device addresses the caller provides (single-process emulation
+    in the tests)."""
+
+    def __init__(self, own: torch.Tensor, bases: list, rank: int, keepalive=None):
+        self.own = own
+        self.world = len(bases)
+        self.rank = rank
+        self.bases = torch.tensor(bases, dtype=torch.int64, device=own.device)
+        self.timeout = torch.zeros(1, dtype=torch.int32, device=own.device)
+        self.epoch = 0
+        self._keep = keepalive
+
+    @classmethod
+    def from_group(cls, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        buf = symm_mem.empty(2 * world * 16, dtype=torch.uint8, device=device)
+        buf.zero_()
+        torch.cuda.synchronize(device)
+        hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        bases = [int(p) for p in hdl.buffer_ptrs]
+        dist.barrier(group)
+        return cls(buf, bases, rank, keepalive=hdl)
+
+    def next_epoch(self) -> tuple[int, int]:
+        prev = self.epoch
+        self.epoch += 1
+        if self.epoch > 0x3FFFFFFF:  # never wraps in practice (one per call)
+            raise RuntimeError("mailbox epoch space exhausted")
+        return self.epoch, prev
+
+    def slots(self, epoch: int) -> int:
+        return self.own.data_ptr() + (epoch & 1) * self.world * 16
+
+    def publish(self, total: torch.Tensor, epoch: int, prev: int) -> None:
+        dev.publish_total(total, self.bases, self.rank, epoch, prev, self.own, self.timeout)
+
+    def check(self) -> None:
+        """Raise if an in-kernel mailbox wait gave up (synchronises)."""
+        if int(self.timeout.item()):
+            raise RuntimeError("mailbox exchange timed out: a peer never published its shard total")
+
+
+class ShardedScan:
+    """Scan a globally contiguous array whose rank-g piece lives on rank g.
+
+    ``exchange``: "nccl" -- one all-gather of the G shard totals between the
+    passes; "p2p" -- the fused exchange over peer memory (MailboxExchange):
+    the reduce's total is stored straight into every peer's mailbox and the
+    consuming kernel waits for its predecessors' totals itself."""
+
+    def __init__(self, group=None, scheme: SchemeId = SchemeId.ACCUMULATE_SCAN_EQUAL, ops=None,
+                 exchange: str = "nccl", mailbox: MailboxExchange | None = None):
         if scheme not in (SchemeId.ACCUMULATE_SCAN_EQUAL, SchemeId.SCAN_INCREMENT_EQUAL):
             raise ValueError("multi-GPU scans use the EQUAL schemes (reduce-then-scan or scan-then-fixup)")
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
         self.group = group
         self.scheme = scheme
         self.ops = ops if ops is not None else CudaOps()
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.exchange = exchange
+        self.mailbox = mailbox
+        if exchange == "p2p" and mailbox is None:
+            self.mailbox = MailboxExchange.from_group(group) if self.world > 1 else None
 
     def _exchange(self, local_total: torch.Tensor) -> torch.Tensor:
         """All-gather of one accumulator per rank (G x 8 bytes)."""
@@ -92,6 +160,8 @@ class ShardedScan:
         and the exchanged shard totals.  Nothing is synchronised."""
         out = shard if out is None else out
         r = self.rank
+        if self.exchange == "p2p" and self.mailbox is not None:
+            return self._call_p2p(shard, out, exclusive, seed, want_total)
         if self.scheme is SchemeId.ACCUMULATE_SCAN_EQUAL:
             totals = self._exchange(self.ops.reduce(shard))
             self.ops.scan(shard, out, exclusive=exclusive, seed=seed, seed_terms=totals[:r] if r else None)
@@ -103,6 +173,28 @@ class ShardedScan:
         if r:
             self.ops.add_offset(out, 0, totals[:r])
         return ShardedScanResult(self.ops.reduce(totals) if want_total else None, totals)
+
+
+    def _call_p2p(self, shard, out, exclusive, seed, want_total):
+        mb = self.mailbox
+        r, g = mb.rank, mb.world
+        e, prev = mb.next_epoch()
+        if self.scheme is SchemeId.ACCUMULATE_SCAN_EQUAL:
+            mb.publish(dev.reduce(shard), e, prev)
+            total = dev.scan_mailbox(shard, out, mb.slots(e), r, e, exclusive=exclusive, seed=seed,
+                                     timeout=mb.timeout)
+        else:
+            local = dev.scan(shard, out, exclusive=exclusive, seed=seed if r == 0 else 0)
+            mb.publish(local, e, prev)
+            if r:
+                delta = dev.scan_mailbox(None, None, mb.slots(e), r, e, timeout=mb.timeout, dtype=shard.dtype)
+                dev.add_offset(out, 0, delta)
+        if not want_total:
+            return ShardedScanResult(None, None)
+        # the global total: seed + every rank's published total (all G slots of epoch e)
+        extra = seed if self.scheme is SchemeId.ACCUMULATE_SCAN_EQUAL else 0
+        tot = dev.scan_mailbox(None, None, mb.slots(e), g, e, seed=extra, timeout=mb.timeout, dtype=shard.dtype)
+        return ShardedScanResult(tot, None)
 
 
 class DistributedScanEngine:

@@ -11,13 +11,14 @@ __global__ void fill_kernel(T *p, int64_t n) {
         p[i] = (T)(i % 3 + 1);
 }
 
-template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP>
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, int MINB = 1>
 void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32_t &epoch, int64_t portion_bytes) {
     using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
-    auto kern = scan_stream_kernel<TIn, TOut, SW, ROWS, NBUF, RWP>;
+    auto kern = scan_stream_kernel<TIn, TOut, SW, ROWS, NBUF, RWP, false, MINB>;
     fill_kernel<TIn><<<1184, 256>>>((TIn *)in, n);
     const int64_t unit = (int64_t)SW * Geo::CHUNK;
     int64_t P = portion_bytes / (int64_t)sizeof(TIn) / unit * unit;
+    if (P < unit) P = unit;
     if (P > (int64_t)Geo::MAXC * Geo::CHUNK) P = (int64_t)Geo::MAXC * Geo::CHUNK / unit * unit;
     const int smem = Geo::smem(P);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
@@ -62,7 +63,7 @@ int main() {
     uint32_t epoch = 0;
     const int64_t N = 1ll << 28;
     run<float, float, 8, 4, 6, 4>("f32_8x4_nb6_r4", in, out, N, scratch, epoch, 32 << 10);
-    run<float, float, 10, 4, 5, 4>("f32_10x4_nb5_r4", in, out, N, scratch, epoch, 40 << 10);
-    run<float, float, 8, 4, 6, 4>("f32_again", in, out, N, scratch, epoch, 32 << 10);
+    run<int64_t, int64_t, 8, 4, 6, 4>("i64_8x4_nb6_r4", in, out, N, scratch, epoch, 32 << 10);
+    run<int64_t, int64_t, 8, 4, 6, 4>("i64_small24", in, out, 1 << 24, scratch, epoch, 32 << 10);
     return 0;
 }

@@ -263,3 +263,31 @@ def test_distributed_engine_single_process_and_validation():
     assert x.tolist() == list(np.cumsum(np.arange(1, 11)))
     with pytest.raises(ValueError):
         eng.run(ScanRequest(data=x, scheme="bogus"))
+
+
+def test_sharded_scan_exchange_validation_and_single_rank():
+    from paper_2312_14874_b200.distributed import ShardedScan
+    with pytest.raises(ValueError):
+        ShardedScan(exchange="carrier-pigeon")
+    s = ShardedScan(exchange="p2p", ops=OracleOps())  # one process: nothing to exchange
+    assert s.mailbox is None
+    x = torch.arange(1, 6, dtype=torch.int64)
+    out = torch.empty_like(x)
+    res = s(x, out)
+    assert out.tolist() == [1, 3, 6, 10, 15] and int(res.total.item()) == 15
+
+
+def test_bench_falls_back_to_nccl_when_p2p_is_unavailable():
+    import bench
+    from paper_2312_14874_b200.plan import SchemeId
+
+    class Fake:
+        def __init__(self, scheme, exchange):
+            if exchange == "p2p":
+                raise RuntimeError("no symmetric memory here")
+            self.exchange = exchange
+
+    obj, label = bench._make_sharded(Fake, SchemeId.ACCUMULATE_SCAN_EQUAL, "p2p", world=4)
+    assert obj.exchange == "nccl" and label.startswith("nccl (p2p unavailable")
+    obj, label = bench._make_sharded(Fake, SchemeId.ACCUMULATE_SCAN_EQUAL, "nccl", world=4)
+    assert label == "nccl"
