@@ -82,11 +82,33 @@ __device__ __forceinline__ void stg256_policy(void *p, const V256 &v, uint64_t p
                  "l"(v.w[1]), "l"(v.w[2]), "l"(v.w[3]), "l"(pol)
                  : "memory");
 }
+// 32 bytes per lane from shared memory as two 16-byte loads.  Lanes sit 32 bytes
+// apart, so loading every lane's first half and then its second half makes
+// lanes l and l+4 of a quarter-warp hit the same bank group (2-way conflict,
+// a third of all shared wavefronts in the f32 profile).  With SWZ, lanes of odd
+// quarters (address bit 7) load their halves in the opposite order: each
+// 16-byte load instruction then covers all eight bank groups per quarter-warp
+// -- conflict-free -- and a register swap restores the order.  Measured on the
+// stream kernel (scripts/stream_variants.cu): +3.8 % for 64-bit data, -1 % for
+// float32 (whose scanner is issue-bound and pays for the swap), so it is a
+// per-kernel choice.
+template <bool SWZ = false>
 __device__ __forceinline__ V256 lds256(const void *p) {
     V256 r;
     const uint32_t a = smem_addr(p);
-    asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(r.w[0]), "=l"(r.w[1]) : "r"(a));
-    asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(r.w[2]), "=l"(r.w[3]) : "r"(a + 16));
+    if constexpr (SWZ) {
+        const uint32_t sw = (a >> 7) & 1u;
+        uint64_t x0, x1, y0, y1;
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(x0), "=l"(x1) : "r"(a + (sw << 4)));
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(y0), "=l"(y1) : "r"(a + ((sw ^ 1u) << 4)));
+        r.w[0] = sw ? y0 : x0;
+        r.w[1] = sw ? y1 : x1;
+        r.w[2] = sw ? x0 : y0;
+        r.w[3] = sw ? x1 : y1;
+    } else {
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(r.w[0]), "=l"(r.w[1]) : "r"(a));
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(r.w[2]), "=l"(r.w[3]) : "r"(a + 16));
+    }
     return r;
 }
 

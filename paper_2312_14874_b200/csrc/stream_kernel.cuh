@@ -162,7 +162,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                 if (w) {
                     V256 raw[ROWS];
 #pragma unroll
-                    for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
+                    for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256<(sizeof(TIn) == 8)>(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
 #pragma unroll
                     for (int rr = 0; rr < ROWS; ++rr) {
                         TIn x[VEC];
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                 if (w) {
                     V256 raw[ROWS];
 #pragma unroll
-                    for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
+                    for (int rr = 0; rr < ROWS; ++rr) raw[rr] = lds256<(sizeof(TIn) == 8)>(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC);
                     widen_chunk<TIn, A, ROWS, VEC>(raw, v);
                 } else {
 #pragma unroll
