@@ -205,11 +205,15 @@ size_t ps_select_scratch_bytes(int64_t n);
  *                1: additionally out[k..n) = rejected values in order (stable partition)
  *   out          device, >= k (partition: n) elements; must not overlap values/flags
  *   count_out    device int64 (nullable) <- k
- * Three launches on `stream` (per-8192-element tile counts, exclusive scan of
- * the counts, scatter through shared memory); the scratch holds the counts
- * only (no look-back descriptors, no epoch). */
+ * Compaction of >= 4 Mi elements with 4/8-byte flags and 16-byte aligned inputs runs in ONE pass
+ * (select_stream.cuh: flags + values loaded once into shared-memory regions,
+ * portion counts exchanged through epoch-tagged descriptors as in ps_scan);
+ * partition mode and small inputs take three launches (per-8192-element tile
+ * counts, exclusive scan of the counts, scatter through shared memory), which
+ * read the flags twice.  epoch as for ps_scan ("select_kernel" tuning knob:
+ * 0 auto, 1 three launches, 2 single pass). */
 int ps_select(const void *values, const void *flags, int64_t n, int dtype_values, int dtype_flags, int partition,
-              void *out, void *count_out, void *scratch, size_t scratch_bytes, void *stream);
+              void *out, void *count_out, void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream);
 
 /* Device workspace for ps_scan_batched_host with chunk_rows rows of cols. */
 size_t ps_scan_batched_host_workspace_bytes(int64_t chunk_rows, int64_t cols, int dtype_in, int dtype_out);
@@ -236,6 +240,7 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "rows_kernel"      batched scans: 0 = auto, 1 = look-back tiles, 2 = one CTA per row
  *   "rounds_min_bytes" auto mode uses the shared-memory-region (stream) kernel from
  *                      this input size (smaller inputs: the look-back kernel)
+ *   "select_kernel"    ps_select: 0 = auto, 1 = three launches, 2 = single pass (compaction)
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability

@@ -51,7 +51,7 @@ SIGNATURES = {
     "ps_scan_mailbox": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _u64, _vp, _i32, _u32, _vp, _vp, _vp, _sz, _u32,
                                _vp]),
     "ps_select_scratch_bytes": (_sz, [_i64]),
-    "ps_select": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "ps_select": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _u32, _vp]),
 }
 
 _lib = None

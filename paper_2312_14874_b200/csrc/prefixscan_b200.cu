@@ -17,6 +17,7 @@
 #include "stream_kernel.cuh"
 #include "rows_kernel.cuh"
 #include "select_kernels.cuh"
+#include "select_stream.cuh"
 
 namespace ps {
 namespace {
@@ -524,6 +525,50 @@ HostLayout host_layout(int64_t chunk, int din, int dout) {
 
 using namespace ps;
 
+namespace ps {
+namespace {
+constexpr int64_t SELECT_STREAM_MIN = 1 << 22;  // elements; below this the 3-launch path wins (fill/drain)
+int g_select_kernel = 0;                         // 0 auto, 1 three launches, 2 single pass
+
+template <typename TV, typename TF>
+int launch_select_stream(const void *values, const void *flags, int64_t n, void *out, void *count, void *scratch,
+                         size_t scratch_bytes, uint32_t epoch, cudaStream_t s) {
+    using Geo = SelectStreamGeom<TV, TF>;
+    auto kern = select_stream_kernel<TV, TF>;
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return PS_ERR_CUDA_BASE + (int)cudaErrorInvalidDevice;
+    if (!per_sm[dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, SS_THREADS, Geo::SMEM);
+        per_sm[dev] = b > 0 ? b : -1;
+    }
+    if (per_sm[dev] <= 0) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
+    int64_t G = (int64_t)per_sm[dev] * device_sms();
+    if (G > 256) G = 256;
+    SelectArgs a{};
+    a.values = values;
+    a.flags = flags;
+    a.out = out;
+    a.n = n;
+    a.portion = SS_P;
+    a.rounds = (n + SS_P * G - 1) / (SS_P * G);
+    a.count = static_cast<long long *>(count);
+    if (!scratch || scratch_bytes < 256 + (size_t)(a.rounds * G) * 16) return PS_ERR_SCRATCH;
+    a.desc = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
+    // the high word makes a stale count (a small integer) in this scratch unmistakable for a tag
+    a.want = ((uint64_t)(~epoch) << 32) | ((uint64_t)epoch << 2);
+    void *params[] = {&a};
+    return cuda_rc(cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)G), dim3(SS_THREADS), params,
+                                               Geo::SMEM, s));
+}
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
 extern "C" {
 
 int ps_version(void) { return 100; }
@@ -574,6 +619,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "rows_kernel")) {
         if (value < 0 || value > 2) return PS_ERR_ARG;
         g_tune.rows_kernel = (int)value;
+    } else if (!std::strcmp(key, "select_kernel")) {
+        if (value < 0 || value > 2) return PS_ERR_ARG;
+        g_select_kernel = (int)value;
     } else if (!std::strcmp(key, "stall_seed")) {
         if (value < 0 || value > 0xffffffffLL) return PS_ERR_ARG;
         g_tune.stall.seed = (uint32_t)value;
@@ -607,6 +655,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "round_ramp")) return g_tune.round_ramp;
     if (!std::strcmp(key, "round_prefetch")) return g_tune.round_prefetch;
     if (!std::strcmp(key, "rows_kernel")) return g_tune.rows_kernel;
+    if (!std::strcmp(key, "select_kernel")) return g_select_kernel;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;
@@ -1006,15 +1055,19 @@ int ps_scan_mailbox(const void *in, void *out, int64_t n, int dtype_in, int dtyp
 size_t ps_select_scratch_bytes(int64_t n) {
     if (n < 0) return 0;
     const int64_t ntiles = (n + SEL_TILE - 1) / SEL_TILE;
-    return 256 + (size_t)ntiles * 8;
+    const size_t counts = 256 + (size_t)ntiles * 8;
+    const size_t desc = 256 + (size_t)(n / SS_P + 256 + 1) * 16;  // single-pass path: <= 256 CTAs
+    return counts > desc ? counts : desc;
 }
 
+
 int ps_select(const void *values, const void *flags, int64_t n, int dtype_values, int dtype_flags, int partition,
-              void *out, void *count_out, void *scratch, size_t scratch_bytes, void *stream) {
+              void *out, void *count_out, void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream) {
     const size_t vb = dsize(dtype_values);
     const size_t fb = dtype_flags == PS_DTYPE_UINT8 ? 1 : dsize(dtype_flags);
     if (!vb || !fb) return PS_ERR_DTYPE;
     if (n < 0 || (partition != 0 && partition != 1)) return PS_ERR_ARG;
+    if (epoch == 0 || epoch > PS_EPOCH_MAX) return PS_ERR_EPOCH;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0) {
         if (count_out) return cuda_rc(cudaMemsetAsync(count_out, 0, 8, s));
@@ -1027,6 +1080,25 @@ int ps_select(const void *values, const void *flags, int64_t n, int dtype_values
     if (overlaps_partially(values, (size_t)n * vb, out, (size_t)n * vb) || values == out) return PS_ERR_OVERLAP;
     if (overlaps_partially(flags, (size_t)n * fb, out, (size_t)n * vb) || flags == out) return PS_ERR_OVERLAP;
     if (!scratch || scratch_bytes < ps_select_scratch_bytes(n)) return PS_ERR_SCRATCH;
+    const bool aligned16 = (uintptr_t)values % 16 == 0 && (uintptr_t)flags % 16 == 0;
+    // auto: the single pass pays off when re-reading the flags is expensive (4/8-byte
+    // flags); byte flags re-read at 1 B/element and the three-launch path, with its
+    // many small CTAs, is faster there (profiles/r01_select_bench.md)
+    if (!partition && aligned16 && g_select_kernel != 1 &&
+        (g_select_kernel == 2 || (n >= SELECT_STREAM_MIN && fb >= 4))) {
+        long long *cnt = count_out ? static_cast<long long *>(count_out) : nullptr;
+#define ONE(TV, TF) return launch_select_stream<TV, TF>(values, flags, n, out, cnt, scratch, scratch_bytes, epoch, s)
+#define BY_F(TV)                        \
+    do {                                \
+        if (fb == 1) ONE(TV, uint8_t);  \
+        if (fb == 4) ONE(TV, uint32_t); \
+        ONE(TV, uint64_t);              \
+    } while (0)
+        if (vb == 4) BY_F(uint32_t);
+        BY_F(uint64_t);
+#undef BY_F
+#undef ONE
+    }
     char *base = static_cast<char *>(scratch);
     long long *total = count_out ? static_cast<long long *>(count_out) : reinterpret_cast<long long *>(base);
     long long *counts = reinterpret_cast<long long *>(base + 256);

@@ -310,9 +310,9 @@ def select(values: torch.Tensor, flags: torch.Tensor, out: torch.Tensor | None =
     if count is None:
         count = torch.empty(1, dtype=torch.int64, device=values.device)
     lib = _lib.load()
-    sptr, sbytes, _ = _scratch_for(values.device, lib.ps_select_scratch_bytes(n), 0, "select")
+    sptr, sbytes, epoch = _scratch_for(values.device, lib.ps_select_scratch_bytes(n), 1, "select")
     rc = lib.ps_select(_ptr(values), _ptr(flags), n, cv, cf, int(bool(partition)), _ptr(out), _ptr(count),
-                       sptr, sbytes, _stream_ptr(values.device))
+                       sptr, sbytes, epoch, _stream_ptr(values.device))
     _lib.check(rc, "ps_select")
     return out, count
 

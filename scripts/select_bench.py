@@ -33,6 +33,8 @@ for fdt, vdt, p in [(torch.int32, torch.int32, 0.5), (torch.uint8, torch.int32, 
         k = int(cnt.item())
         fb, vb = f.element_size(), v.element_size()
         alg = n * (fb + vb) + (n if partition else k) * vb
-        moved = n * fb + alg
+        single = (not partition) and fb >= 4  # ps_select's auto choice (single pass) -> flags read once
+        moved = alg + (0 if single else n * fb)
         print(f"flags {str(fdt):12s} values {str(vdt):12s} p={p:<5} {'partition' if partition else 'select   '} "
+              f"{'1-pass' if single else '3-launch'} "
               f"{t * 1e3:8.1f} us  alg {alg / t / 1e6:7.1f} GB/s  moved {moved / t / 1e6:7.1f} GB/s")

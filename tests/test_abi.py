@@ -98,18 +98,20 @@ def test_select_validation_without_gpu(lib):
     from paper_2312_14874_b200 import _lib
     buf = ctypes.create_string_buffer(256)
     # unsupported value / flag dtypes, bad mode, negative n, missing buffers, short scratch
-    assert lib.ps_select(buf, buf, 4, 7, 1, 0, buf, None, buf, 256, None) == _lib.PS_ERR_DTYPE
-    assert lib.ps_select(buf, buf, 4, 1, 9, 0, buf, None, buf, 256, None) == _lib.PS_ERR_DTYPE
-    assert lib.ps_select(buf, buf, 4, 1, 1, 2, buf, None, buf, 256, None) == _lib.PS_ERR_ARG
-    assert lib.ps_select(buf, buf, -1, 1, 1, 0, buf, None, buf, 256, None) == _lib.PS_ERR_ARG
-    assert lib.ps_select(None, buf, 4, 1, 1, 0, buf, None, buf, 256, None) == _lib.PS_ERR_ARG
+    assert lib.ps_select(buf, buf, 4, 7, 1, 0, buf, None, buf, 256, 1, None) == _lib.PS_ERR_DTYPE
+    assert lib.ps_select(buf, buf, 4, 1, 9, 0, buf, None, buf, 256, 1, None) == _lib.PS_ERR_DTYPE
+    assert lib.ps_select(buf, buf, 4, 1, 1, 2, buf, None, buf, 256, 1, None) == _lib.PS_ERR_ARG
+    assert lib.ps_select(buf, buf, -1, 1, 1, 0, buf, None, buf, 256, 1, None) == _lib.PS_ERR_ARG
+    assert lib.ps_select(buf, buf, 4, 1, 1, 0, buf, None, buf, 256, 0, None) == _lib.PS_ERR_EPOCH
+    assert lib.ps_select(None, buf, 4, 1, 1, 0, buf, None, buf, 256, 1, None) == _lib.PS_ERR_ARG
     a = ctypes.create_string_buffer(1 << 16)
     b = ctypes.create_string_buffer(1 << 16)
     c = ctypes.create_string_buffer(1 << 16)
-    assert lib.ps_select(a, b, 16, 1, 1, 0, a, None, c, 1 << 16, None) == _lib.PS_ERR_OVERLAP
-    assert lib.ps_select(a, b, 16, 1, 1, 0, c, None, a, 8, None) == _lib.PS_ERR_SCRATCH
-    # scratch: 256 bytes of control + one int64 count per 8192-element tile
-    assert lib.ps_select_scratch_bytes(0) == 256
-    assert lib.ps_select_scratch_bytes(8192) == 256 + 8
-    assert lib.ps_select_scratch_bytes(8193) == 256 + 16
+    assert lib.ps_select(a, b, 16, 1, 1, 0, a, None, c, 1 << 16, 1, None) == _lib.PS_ERR_OVERLAP
+    assert lib.ps_select(a, b, 16, 1, 1, 0, c, None, a, 8, 1, None) == _lib.PS_ERR_SCRATCH
+    # scratch: the larger of the tile counts (8 bytes per 8192 elements) and the
+    # single-pass descriptors (16 bytes per 4096-element portion, + one round of slack)
+    assert lib.ps_select_scratch_bytes(0) == 256 + 257 * 16
+    big = lib.ps_select_scratch_bytes(1 << 28)
+    assert big == 256 + ((1 << 28) // 4096 + 257) * 16
     assert lib.ps_select_scratch_bytes(-1) == 0

@@ -150,3 +150,75 @@ def test_select_full_size_cfg3_flags():
     rej = out[k:]
     assert bool((rej[1:] > rej[:-1]).all().item())
     assert bool((f[rej.long()] == 0).all().item())
+
+
+@pytest.fixture
+def select_kernel():
+    from paper_2312_14874_b200 import _lib
+    lib = _lib.load()
+    prev = lib.ps_get_tuning(b"select_kernel")
+
+    def set_(k):
+        assert lib.ps_set_tuning(b"select_kernel", k) == 0
+
+    yield set_
+    lib.ps_set_tuning(b"select_kernel", prev)
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 148 * 4096 - 3, 148 * 4096 + 5, 3 * 148 * 4096 + 4099, 5_000_011])
+def test_single_pass_select_sizes(select_kernel, n):
+    from paper_2312_14874_b200 import device as dev
+    select_kernel(2)
+    v = _values(n, np.int32, n)
+    f = _flags(n, np.int32, 0.5, n)
+    out, count = dev.select(_dev(v), _dev(f))
+    want = v[f != 0]
+    assert int(count.item()) == want.size
+    assert np.array_equal(out.cpu().numpy()[:want.size], want)
+
+
+@pytest.mark.parametrize("vdt", [np.int32, np.float32, np.int64, np.float64])
+@pytest.mark.parametrize("fdt", [np.bool_, np.int32, np.int64])
+@pytest.mark.parametrize("p", [0.0, 0.3, 1.0])
+def test_single_pass_select_dtypes(select_kernel, vdt, fdt, p):
+    from paper_2312_14874_b200 import device as dev
+    select_kernel(2)
+    n = 2 * 148 * 4096 + 777
+    v = _values(n, vdt, 5)
+    f = _flags(n, fdt, p, 5)
+    out, count = dev.select(_dev(v), _dev(f))
+    want = v[f != 0]
+    assert int(count.item()) == want.size
+    assert np.array_equal(out.cpu().numpy()[:want.size].view(np.uint8), want.view(np.uint8))
+
+
+def test_single_pass_matches_three_launch_and_repeats(select_kernel):
+    """Both paths agree bit for bit, and repeated single-pass calls (fresh epochs on
+    a scratch that also held tile counts) stay correct."""
+    from paper_2312_14874_b200 import device as dev
+    n = 6_000_001
+    v = _dev(_values(n, np.float32, 8))
+    f = _dev(_flags(n, np.uint8, 0.37, 8))
+    select_kernel(1)
+    a, ca = dev.select(v, f)
+    a = a[:int(ca.item())].clone()
+    select_kernel(2)
+    for _ in range(4):
+        b, cb = dev.select(v, f)
+        assert int(cb.item()) == a.numel()
+        assert torch.equal(b[:a.numel()], a)
+        select_kernel(1)
+        dev.select(v, f)  # leaves tile counts in the shared scratch
+        select_kernel(2)
+
+
+def test_single_pass_misaligned_falls_back(select_kernel):
+    from paper_2312_14874_b200 import device as dev
+    select_kernel(2)
+    n = 1_000_000
+    v = _values(n + 3, np.int32, 2)
+    f = _flags(n + 3, np.int32, 0.5, 2)
+    out, count = dev.select(_dev(v)[1:n + 1], _dev(f)[3:n + 3])  # 4-byte offsets: not 16-byte aligned
+    want = v[1:n + 1][f[3:n + 3] != 0]
+    assert int(count.item()) == want.size
+    assert np.array_equal(out.cpu().numpy()[:want.size], want)
