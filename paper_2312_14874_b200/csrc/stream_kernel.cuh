@@ -130,6 +130,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                 const int b = (int)(r % NBUF);
                 stall_site<STALL>(a.stall, r * G + c, 0, 1);
                 if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
+#ifdef PS_TRACE
+                if (g_trace && true) g_trace[(r * G + c) * 8 + 0] = gtimer();
+#endif
                 if (whole(r)) {
                     constexpr uint32_t PIECE = 16384;
                     const uint32_t bytes = (uint32_t)(P * sizeof(TIn));
@@ -152,6 +155,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
             mbar_wait(&full[b], par(r));
+#ifdef PS_TRACE
+                if (g_trace && rw == 0 && lane == 0) g_trace[(r * G + c) * 8 + 1] = gtimer();
+#endif
             stall_site<STALL>(a.stall, r * G + c, rw, 2);
             A *tot = chunk_tot + b * MAXC;
             const TIn *sb = buf + (size_t)b * P;
@@ -191,6 +197,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                 if (lane == 0) {
                     st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
                     mbar_arrive(&red[b]);
+#ifdef PS_TRACE
+                if (g_trace && true) g_trace[(r * G + c) * 8 + 2] = gtimer();
+#endif
                 }
             }
             named_sync(BAR_RED, RT);
@@ -217,7 +226,13 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
 #ifdef PS_EXP_NOLEDGER
             sb = sa = (A)0;
 #else
+#ifdef PS_TRACE
+            if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 3] = gtimer();
+#endif
             gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
+#ifdef PS_TRACE
+                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
+#endif
 #endif
 
             mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
@@ -242,6 +257,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             stall_site<STALL>(a.stall, r * G + c, 0, 5);
             __syncwarp();
             if (lane == 0) mbar_arrive(&pre[b]);
+#ifdef PS_TRACE
+                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
+#endif
         }
         if (c == 0 && lane == 0 && a.total) *reinterpret_cast<A *>(a.total) = carry;
         return;
@@ -252,6 +270,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
     for (int64_t r = 0; r < a.rounds; ++r) {
         const int b = (int)(r % NBUF);
         mbar_wait(&pre[b], par(r));
+#ifdef PS_TRACE
+                if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 6] = gtimer();
+#endif
         stall_site<STALL>(a.stall, r * G + c, warp, 6);
         const A *pr = chunk_pre + b * MAXC;
         const TIn *sb = buf + (size_t)b * P;
@@ -332,6 +353,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&freeb[b]);
+#ifdef PS_TRACE
+                if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 7] = gtimer();
+#endif
     }
 }
 

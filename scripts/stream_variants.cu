@@ -68,7 +68,6 @@ int main() {
     run<float, float, 8, 4, 6, 4>("f32_28", in, out, N, scratch, epoch, 32 << 10);
     run<int64_t, int64_t, 8, 4, 6, 4>("i64_28", in, out, N, scratch, epoch, 32 << 10);
     run<int, int64_t, 8, 4, 6, 4>("i32_28", in, out, N, scratch, epoch, 32 << 10);
-    run<int64_t, int64_t, 8, 4, 6, 4>("i64_24", in, out, S, scratch, epoch, 32 << 10);
     run<float, float, 8, 4, 6, 4>("f32_28_again", in, out, N, scratch, epoch, 32 << 10);
     return 0;
 }
