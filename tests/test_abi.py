@@ -115,3 +115,33 @@ def test_select_validation_without_gpu(lib):
     big = lib.ps_select_scratch_bytes(1 << 28)
     assert big == 256 + ((1 << 28) // 4096 + 257) * 16
     assert lib.ps_select_scratch_bytes(-1) == 0
+
+
+def test_mailbox_exchange_validation_without_gpu(lib):
+    from paper_2312_14874_b200 import _lib
+    buf = ctypes.create_string_buffer(256)
+    # ps_publish_total: total, peer_mailboxes, n_peers, rank, epoch, prev_epoch, own_mailbox, timeout, stream
+    assert lib.ps_publish_total(None, buf, 2, 0, 1, 0, buf, None, None) == _lib.PS_ERR_ARG
+    assert lib.ps_publish_total(buf, buf, 0, 0, 1, 0, buf, None, None) == _lib.PS_ERR_ARG
+    assert lib.ps_publish_total(buf, buf, 2, 2, 1, 0, buf, None, None) == _lib.PS_ERR_ARG   # rank out of range
+    assert lib.ps_publish_total(buf, buf, 2, 1, 1, 1, buf, None, None) == _lib.PS_ERR_EPOCH  # prev == epoch
+    assert lib.ps_publish_total(buf, buf, 2, 1, 0, 0, buf, None, None) == _lib.PS_ERR_EPOCH
+    assert lib.ps_publish_total(buf, buf, 2, 1, 2, 1, None, None, None) == _lib.PS_ERR_ARG  # prev needs own mailbox
+    # ps_scan_mailbox: in, out, n, din, dout, excl, seed, mailbox, n_wait, mail_epoch, timeout, total, scratch,
+    #                  scratch_bytes, epoch, stream
+    assert lib.ps_scan_mailbox(buf, buf, 4, 5, 2, 0, 0, buf, 1, 1, None, None, buf, 256, 1, None) == _lib.PS_ERR_DTYPE
+    assert lib.ps_scan_mailbox(buf, buf, 4, 2, 2, 0, 0, None, 1, 1, None, None, buf, 256, 1, None) == _lib.PS_ERR_ARG
+    assert lib.ps_scan_mailbox(buf, buf, 4, 2, 2, 0, 0, buf, 1, 0, None, None, buf, 256, 1, None) == _lib.PS_ERR_EPOCH
+    assert lib.ps_scan_mailbox(buf, buf, -1, 2, 2, 0, 0, buf, 1, 1, None, None, buf, 256, 1, None) == _lib.PS_ERR_ARG
+
+
+def test_tuning_knobs_roundtrip(lib):
+    from paper_2312_14874_b200 import _lib
+    for key, good, bad in ((b"scan_kernel", 3, 4), (b"rows_kernel", 2, 3), (b"select_kernel", 2, 3),
+                           (b"stall_prob", 1024, 1025)):
+        prev = lib.ps_get_tuning(key)
+        assert lib.ps_set_tuning(key, good) == 0 and lib.ps_get_tuning(key) == good
+        assert lib.ps_set_tuning(key, bad) == _lib.PS_ERR_ARG and lib.ps_get_tuning(key) == good
+        assert lib.ps_set_tuning(key, prev) == 0
+    assert lib.ps_get_tuning(b"no_such_knob") == -1
+    assert lib.ps_set_tuning(b"no_such_knob", 1) == _lib.PS_ERR_ARG
