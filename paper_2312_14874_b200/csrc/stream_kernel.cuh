@@ -269,7 +269,10 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
     const uint64_t pol = policy_evict_first();
     for (int64_t r = 0; r < a.rounds; ++r) {
         const int b = (int)(r % NBUF);
-        mbar_wait(&pre[b], par(r));
+        // everything that does not need the carry (loads, widening, in-lane and
+        // warp scans) runs as soon as the data has landed, overlapping the
+        // ledger's grid-wide exchange; only the carry adds and stores wait for it
+        mbar_wait(&full[b], par(r));
 #ifdef PS_TRACE
                 if (g_trace && warp == 0 && lane == 0) g_trace[(r * G + c) * 8 + 6] = gtimer();
 #endif
@@ -312,18 +315,23 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                         if (lane >= d) sc[rr] += y;
                     }
                 }
+                A exs[ROWS], rts[ROWS];
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) {
+                    if constexpr (FLOAT) {
+                        exs[rr] = shfl_up(sc[rr], 1);
+                        if (lane == 0) exs[rr] = (A)0;
+                    } else {
+                        exs[rr] = sc[rr] - v[rr][VEC - 1];
+                    }
+                    rts[rr] = shfl_idx(sc[rr], 31);
+                }
+                mbar_wait(&pre[b], par(r));  // the chunk carries of region r (the ledger)
                 A base = pr[ch];
 #pragma unroll
                 for (int rr = 0; rr < ROWS; ++rr) {
-                    A ex;
-                    if constexpr (FLOAT) {
-                        ex = shfl_up(sc[rr], 1);
-                        if (lane == 0) ex = (A)0;
-                    } else {
-                        ex = sc[rr] - v[rr][VEC - 1];
-                    }
-                    const A bb = base + ex;
-                    base += shfl_idx(sc[rr], 31);
+                    const A bb = base + exs[rr];
+                    base += rts[rr];
                     TOut y[VEC];
                     if (a.exclusive) {
                         y[0] = (TOut)bb;

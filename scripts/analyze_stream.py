@@ -15,8 +15,8 @@ for name in sys.argv[1:] or ["f32", "i64"]:
     print(" gather end - last publish  :", q(ge - pub.max(axis=1)[:, None]))
     print(" last publish - first publ. :", q(pub.max(axis=1) - pub.min(axis=1)))
     print(" gather end -> carries      :", q(pre - ge))
-    print(" carries -> scanner start   :", q(s0 - pre))
-    print(" scanner duration (warp 0)  :", q(s1 - s0))
+    print(" carries - scanner data-ready:", q(pre - s0))
+    print(" scanner data-ready -> done :", q(s1 - s0))
     print(" scanner done -> next issue :", q(iss[6:] - s1[:-6]))
     print(" region period (max publish):", q(np.diff(pub.max(axis=1))))
     print(" buffer cycle (issue->issue):", q(iss[6:] - iss[:-6]))

@@ -49,32 +49,42 @@ int main(int argc, char **argv) {
     g_scratch_bytes = 256 << 20;
     CK(cudaMalloc(&g_scratch, g_scratch_bytes));
     CK(cudaMemset(g_scratch, 0, g_scratch_bytes));
-    Case cases[] = {
-        {"cfg1 i64", 1ll << 24, PS_DTYPE_INT64, PS_DTYPE_INT64, 0, 8, 8},
-        {"cfg2 f32", 1ll << 28, PS_DTYPE_FLOAT32, PS_DTYPE_FLOAT32, 0, 4, 4},
-        {"cfg3 i32>i64 ex", 1ll << 28, PS_DTYPE_INT32, PS_DTYPE_INT64, 1, 4, 8},
-        {"2^28 i64", 1ll << 28, PS_DTYPE_INT64, PS_DTYPE_INT64, 0, 8, 8},
+    struct Pair { const char *name; int di, dout, ei, eo; };
+    const Pair pairs[] = {
+        {"int32 -> int32", PS_DTYPE_INT32, PS_DTYPE_INT32, 4, 4},
+        {"int32 -> int64", PS_DTYPE_INT32, PS_DTYPE_INT64, 4, 8},
+        {"int64 -> int64", PS_DTYPE_INT64, PS_DTYPE_INT64, 8, 8},
+        {"uint32 -> uint32", PS_DTYPE_UINT32, PS_DTYPE_UINT32, 4, 4},
+        {"uint32 -> uint64", PS_DTYPE_UINT32, PS_DTYPE_UINT64, 4, 8},
+        {"uint64 -> uint64", PS_DTYPE_UINT64, PS_DTYPE_UINT64, 8, 8},
+        {"float32 -> float32", PS_DTYPE_FLOAT32, PS_DTYPE_FLOAT32, 4, 4},
+        {"float32 -> float64", PS_DTYPE_FLOAT32, PS_DTYPE_FLOAT64, 4, 8},
+        {"float64 -> float64", PS_DTYPE_FLOAT64, PS_DTYPE_FLOAT64, 8, 8},
     };
-    const int64_t rbs[] = {32ll << 20, 40ll << 20, 48ll << 20, 64ll << 20, 80ll << 20};
-    for (const Case &c : cases) {
-        PK(ps_set_tuning("scan_kernel", 1));
-        double ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
-        double gb = (double)c.n * (c.ei + c.eo) / 1e9;
-        printf("%-16s lookback            %8.1f us %7.1f GB/s\n", c.name, ms * 1e3, gb / (ms * 1e-3));
-        PK(ps_set_tuning("scan_kernel", 3));
-        ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
-        printf("%-16s stream (smem regions) %8.1f us %7.1f GB/s\n", c.name, ms * 1e3, gb / (ms * 1e-3));
-        PK(ps_set_tuning("scan_kernel", 2));
-        for (int lead : {1, 2})
-            for (int64_t rb : rbs) {
-                PK(ps_set_tuning("round_bytes", rb));
-                PK(ps_set_tuning("round_lead", lead));
-                ms = time_scan(in, out, c.n, c.di, c.dout, c.excl, 10);
-                printf("%-16s rounds lead=%d R=%3lld MiB %8.1f us %7.1f GB/s\n", c.name, lead, (long long)(rb >> 20),
-                       ms * 1e3, gb / (ms * 1e-3));
+    printf("| pair | n | auto kernel | us | GB/s | look-back GB/s | L2-rounds GB/s | stream GB/s |\n");
+    printf("|---|---|---|---|---|---|---|---|\n");
+    for (const Pair &p : pairs) {
+        for (int lg : {20, 24, 28}) {
+            const int64_t n = 1ll << lg;
+            const double gb = (double)n * (p.ei + p.eo) / 1e9;
+            PK(ps_set_tuning("scan_kernel", 0));
+            const double ms = time_scan(in, out, n, p.di, p.dout, 0, 20);
+            const bool big = n * p.ei >= ps_get_tuning("rounds_min_bytes");
+            double k[3] = {0, 0, 0};
+            if (lg == 28) {
+                for (int i = 0; i < 3; ++i) {
+                    PK(ps_set_tuning("scan_kernel", i + 1));
+                    k[i] = gb / (time_scan(in, out, n, p.di, p.dout, 0, 10) * 1e-3);
+                }
+                PK(ps_set_tuning("scan_kernel", 0));
             }
-        PK(ps_set_tuning("round_lead", 2));
-        PK(ps_set_tuning("round_bytes", 0));
+            if (lg == 28)
+                printf("| %s | 2^%d | %s | %.1f | %.0f | %.0f | %.0f | %.0f |\n", p.name, lg, big ? "stream" : "look-back",
+                       ms * 1e3, gb / (ms * 1e-3), k[0], k[1], k[2]);
+            else
+                printf("| %s | 2^%d | %s | %.1f | %.0f | | | |\n", p.name, lg, big ? "stream" : "look-back", ms * 1e3,
+                       gb / (ms * 1e-3));
+        }
     }
     return 0;
 }

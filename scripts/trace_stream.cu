@@ -1,7 +1,7 @@
 // scripts/trace_stream.cu -- per-(region, CTA) timeline of scan_stream_kernel (dev tool).
 // gpurun_out/trace_stream_<name>.bin: 8 uint64 per (region, CTA):
 //   [0] TMA issued [1] data landed (reducer) [2] portion total published [3] ledger gather start
-//   [4] gather done [5] carries ready [6] scanner warp 0 starts [7] scanner warp 0 done
+//   [4] gather done [5] carries ready [6] scanner warp 0 sees its data [7] scanner warp 0 done
 #define PS_TRACE 1
 #include <cstdio>
 #include <cstdlib>
