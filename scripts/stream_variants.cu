@@ -29,7 +29,7 @@ void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32
     int per = 0, sms = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, Geo::THREADS, smem));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    const int64_t G = (int64_t)per * sms;
+    const int64_t G = getenv("GRID") ? atoll(getenv("GRID")) : (int64_t)per * sms;
     StreamArgs a{};
     a.in = in; a.out = out; a.lo = 0; a.hi = n; a.portion = P;
     a.rounds = (n + P * G - 1) / (P * G);

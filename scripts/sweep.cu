@@ -61,6 +61,24 @@ int main(int argc, char **argv) {
         {"float32 -> float64", PS_DTYPE_FLOAT32, PS_DTYPE_FLOAT64, 4, 8},
         {"float64 -> float64", PS_DTYPE_FLOAT64, PS_DTYPE_FLOAT64, 8, 8},
     };
+    if (argc > 1 && !strcmp(argv[1], "threshold")) {
+        printf("| pair | n (bytes in) | look-back us | stream us | L2-rounds us |\n|---|---|---|---|---|\n");
+        for (const Pair &p : pairs) {
+            if (p.di != PS_DTYPE_INT64 && p.di != PS_DTYPE_FLOAT32 && !(p.di == PS_DTYPE_INT32 && p.dout == PS_DTYPE_INT64)) continue;
+            for (int lg = 18; lg <= 25; ++lg) {
+                const int64_t n = (1ll << lg) / p.ei * 4;  // 2^lg * 4 bytes of input
+                double t[3];
+                for (int k = 0; k < 3; ++k) {
+                    PK(ps_set_tuning("scan_kernel", k == 0 ? 1 : (k == 1 ? 3 : 2)));
+                    t[k] = time_scan(in, out, n, p.di, p.dout, 0, 20) * 1e3;
+                }
+                printf("| %s | %lld (%lld KiB) | %.1f | %.1f | %.1f |\n", p.name, (long long)n,
+                       (long long)(n * p.ei >> 10), t[0], t[1], t[2]);
+            }
+        }
+        PK(ps_set_tuning("scan_kernel", 0));
+        return 0;
+    }
     printf("| pair | n | auto kernel | us | GB/s | look-back GB/s | L2-rounds GB/s | stream GB/s |\n");
     printf("|---|---|---|---|---|---|---|---|\n");
     for (const Pair &p : pairs) {

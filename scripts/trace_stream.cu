@@ -51,5 +51,6 @@ int main() {
     uint32_t epoch = 0;
     run<float, float, 8, 4, 6, 4>("f32", in, out, 1ll << 28, scratch, epoch);
     run<int64_t, int64_t, 8, 4, 6, 4>("i64", in, out, 1ll << 27, scratch, epoch);
+    run<int64_t, int64_t, 8, 4, 6, 4>("i64_cfg1", in, out, 1ll << 24, scratch, epoch);
     return 0;
 }
