@@ -51,7 +51,7 @@ struct StreamGeom {
     static constexpr int VEC = 32 / sizeof(TIn);
     static constexpr int ROW_ELEMS = 32 * VEC;
     static constexpr int CHUNK = ROWS * ROW_ELEMS;  // one warp's unit (ROWS KiB)
-    static constexpr int MAXC = 64;                 // chunks per portion
+    static constexpr int MAXC = 16;                 // chunks per portion (32 KiB portions hold 8)
     static constexpr int BUF_BYTES_MAX = 200 * 1024;
     static constexpr int SMEM_FIXED = 4 * NBUF * 8 + 2 * NBUF * MAXC * 8 + 128;
     static constexpr int smem(int64_t portion) { return (int)(NBUF * portion * sizeof(TIn)) + SMEM_FIXED; }
