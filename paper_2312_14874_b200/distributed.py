@@ -100,7 +100,24 @@ class MailboxExchange:
         hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
         bases = [int(p) for p in hdl.buffer_ptrs]
         dist.barrier(group)
-        return cls(buf, bases, rank, keepalive=hdl)
+        ex = cls(buf, bases, rank, keepalive=hdl)
+        ex.self_test(group)
+        return ex
+
+    def self_test(self, group=None) -> None:
+        """One exchange of known values (rank + 1) through the real protocol;
+        raises unless every rank sees the exact sum, so a broken peer mapping
+        is caught at setup (callers fall back to the NCCL all-gather)."""
+        e, prev = self.next_epoch()
+        mine = torch.tensor([self.rank + 1], dtype=torch.int64, device=self.own.device)
+        self.publish(mine, e, prev)
+        got = dev.scan_mailbox(None, None, self.slots(e), self.world, e, timeout=self.timeout, dtype=torch.int64)
+        ok = int(got.item()) == self.world * (self.world + 1) // 2 and int(self.timeout.item()) == 0
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=self.own.device)
+        if dist.is_initialized():
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not int(flag.item()):
+            raise RuntimeError("mailbox exchange self-test failed")
 
     def next_epoch(self) -> tuple[int, int]:
         prev = self.epoch

@@ -103,3 +103,17 @@ def test_p2p_under_stalls():
             assert np.array_equal(np.concatenate([o.cpu().numpy() for o in outs]), np.cumsum(a))
     for g in range(G):
         ex[g].check()
+
+
+def test_mailbox_self_test_emulated():
+    """The setup self-test (publish rank+1, fold all slots) on emulated ranks:
+    run rank 0's publish, then rank 1's, then both folds."""
+    from paper_2312_14874_b200 import device as dev
+    ex = _exchanges(2)
+    for g in range(2):
+        e, prev = ex[g].next_epoch()
+        ex[g].publish(torch.tensor([g + 1], dtype=torch.int64, device="cuda"), e, prev)
+    for g in range(2):
+        got = dev.scan_mailbox(None, None, ex[g].slots(1), 2, 1, timeout=ex[g].timeout, dtype=torch.int64)
+        assert int(got.item()) == 3
+        ex[g].check()
