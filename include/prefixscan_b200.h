@@ -164,6 +164,16 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
                  int exclusive, uint64_t seed_bits, void *total_host, void *workspace,
                  size_t workspace_bytes, int64_t chunk_elems, uint32_t epoch, void *stream);
 
+/* Blelloch tree step functions on a power-of-two span, in place, element-typed
+ * arithmetic in the reference's exact pairing (bit-identical float results):
+ *   ps_tree_up_sweep   <- up_sweep   simd.py:327-334, :356-360 (root -> *root_out,
+ *                         device, element-typed, nullable)
+ *   ps_tree_down_sweep <- down_sweep simd.py:338-347, :363-367 (up-swept span ->
+ *                         its exclusive scan)
+ * PS_ERR_ARG unless n is a power of two (simd.py:370-372). */
+int ps_tree_up_sweep(void *data, int64_t n, int dtype, void *root_out, void *stream);
+int ps_tree_down_sweep(void *data, int64_t n, int dtype, void *stream);
+
 /* Fused exchange of shard totals over NVLink / NVSwitch (SURVEY.md §8(e) option ii;
  * replaces the all-gather feeding the ledger fold, engine.py:329-331, across
  * GPUs).  Every GPU owns a mailbox of 2 x n_peers 16-byte slots (e.g. in

@@ -222,6 +222,18 @@ def vertical_scan(data: np.ndarray, start: int, length: int, offset=0, w: int = 
     return int(acc) if acc_dt == np.uint64 else float(acc)
 
 
+def up_sweep(data: np.ndarray, start: int, length: int):
+    """simd.py:327-334 / :356-360: in-place up-sweep; returns the root (element dtype)."""
+    root = np.zeros(1, data.dtype)
+    _check(lib().or_up_sweep(_code(data), _ptr(data), start, length, _ptr(root)), "up")
+    return root[0]
+
+
+def down_sweep(data: np.ndarray, start: int, length: int) -> None:
+    """simd.py:338-347 / :363-367: in-place down-sweep."""
+    _check(lib().or_down_sweep(_code(data), _ptr(data), start, length), "down")
+
+
 def tree_scan(data: np.ndarray, start: int, length: int, offset=0):
     """simd.py:375-395: up-sweep, down-sweep, add-back (in place)."""
     scratch = data[start:start + length].copy()

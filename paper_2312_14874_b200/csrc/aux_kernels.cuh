@@ -89,3 +89,81 @@ __global__ void wrapped_block_total_kernel(const uint32_t *in, int64_t n, int w,
 }
 
 }  // namespace ps
+
+namespace ps {
+
+// ---- Blelloch tree step functions: up_sweep / down_sweep (simd.py:327-367) ---------------
+// Element-typed arithmetic (uint32 wraps, float32 adds in float32) in exactly the
+// reference's pairing, so float results are bit-identical.  Levels with stride
+// below TREE_B run inside one CTA's shared-memory block; the top levels (a
+// handful for any n) run one launch each.
+constexpr int TREE_B = 2048;
+constexpr int TREE_THREADS = 1024;
+
+template <typename T>
+__device__ __forceinline__ T tree_add(T a, T b) {
+    return (T)(a + b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TREE_THREADS) tree_up_block_kernel(T *d, int64_t n, int64_t blk) {
+    __shared__ T s[TREE_B];
+    T *base = d + (int64_t)blockIdx.x * blk;
+    for (int i = threadIdx.x; i < blk; i += TREE_THREADS) s[i] = base[i];
+    __syncthreads();
+    for (int stride = 1; stride < blk; stride *= 2) {
+        const int step = stride * 2;
+        for (int k = threadIdx.x; (int64_t)(k + 1) * step - 1 < blk; k += TREE_THREADS) {
+            const int i = (k + 1) * step - 1;
+            s[i] = tree_add(s[i], s[i - stride]);
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < blk; i += TREE_THREADS) base[i] = s[i];
+}
+
+template <typename T>
+__global__ void tree_up_level_kernel(T *d, int64_t n, int64_t stride) {
+    const int64_t step = stride * 2;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; (k + 1) * step - 1 < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = (k + 1) * step - 1;
+        d[i] = tree_add(d[i], d[i - stride]);
+    }
+}
+
+template <typename T>
+__global__ void tree_down_level_kernel(T *d, int64_t n, int64_t stride, int clear_root) {
+    const int64_t step = stride * 2;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; (k + 1) * step - 1 < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = (k + 1) * step - 1;
+        const T t = d[i - stride];
+        const T top = (clear_root && i == n - 1) ? (T)0 : d[i];
+        d[i - stride] = top;
+        d[i] = tree_add(top, t);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TREE_THREADS) tree_down_block_kernel(T *d, int64_t n, int64_t blk, int clear_root) {
+    __shared__ T s[TREE_B];
+    T *base = d + (int64_t)blockIdx.x * blk;
+    for (int i = threadIdx.x; i < blk; i += TREE_THREADS) s[i] = base[i];
+    __syncthreads();
+    if (clear_root && threadIdx.x == 0) s[blk - 1] = (T)0;  // n <= TREE_B: the root lives here
+    __syncthreads();
+    for (int stride = (int)(blk / 2); stride >= 1; stride /= 2) {
+        const int step = stride * 2;
+        for (int k = threadIdx.x; (int64_t)(k + 1) * step - 1 < blk; k += TREE_THREADS) {
+            const int i = (k + 1) * step - 1;
+            const T t = s[i - stride];
+            s[i - stride] = s[i];
+            s[i] = tree_add(s[i], t);
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < blk; i += TREE_THREADS) base[i] = s[i];
+}
+
+}  // namespace ps

@@ -1010,6 +1010,54 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
     return cuda_rc(e);
 }
 
+// ---- Blelloch tree step functions (simd.py:327-367) -------------------------------------------
+int ps_tree_up_sweep(void *data, int64_t n, int dtype, void *root_out, void *stream) {
+    if (!dsize(dtype)) return PS_ERR_DTYPE;
+    if (n < 1 || (n & (n - 1)) || !data) return PS_ERR_ARG;  // power-of-two span (simd.py:370-372)
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t blk = n < TREE_B ? n : TREE_B;
+    const int64_t nblk = n / blk;
+    if (nblk > 0x7fffffffLL) return PS_ERR_ARG;
+#define CALL(T)                                                                                                   \
+    do {                                                                                                          \
+        T *d = static_cast<T *>(data);                                                                            \
+        tree_up_block_kernel<T><<<(unsigned)nblk, TREE_THREADS, 0, s>>>(d, n, blk);                                \
+        for (int64_t st = blk; st < n; st *= 2) {                                                                 \
+            const int64_t work = n / (2 * st);                                                                    \
+            tree_up_level_kernel<T><<<(unsigned)((work + 255) / 256 < 148 * 16 ? (work + 255) / 256 : 148 * 16),     \
+                                      256, 0, s>>>(d, n, st);                                                      \
+        }                                                                                                         \
+        if (root_out) cudaMemcpyAsync(root_out, d + n - 1, sizeof(T), cudaMemcpyDeviceToDevice, s);               \
+    } while (0)
+    PS_DISPATCH_ONE(dtype, CALL);
+#undef CALL
+    return launch_rc();
+}
+
+int ps_tree_down_sweep(void *data, int64_t n, int dtype, void *stream) {
+    if (!dsize(dtype)) return PS_ERR_DTYPE;
+    if (n < 1 || (n & (n - 1)) || !data) return PS_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t blk = n < TREE_B ? n : TREE_B;
+    const int64_t nblk = n / blk;
+    if (nblk > 0x7fffffffLL) return PS_ERR_ARG;
+#define CALL(T)                                                                                                   \
+    do {                                                                                                          \
+        T *d = static_cast<T *>(data);                                                                            \
+        int clear = 1;                                                                                            \
+        for (int64_t st = n / 2; st >= blk; st /= 2) {                                                            \
+            const int64_t work = n / (2 * st);                                                                    \
+            tree_down_level_kernel<T><<<(unsigned)((work + 255) / 256 < 148 * 16 ? (work + 255) / 256 : 148 * 16),   \
+                                        256, 0, s>>>(d, n, st, clear);                                             \
+            clear = 0;                                                                                            \
+        }                                                                                                         \
+        tree_down_block_kernel<T><<<(unsigned)nblk, TREE_THREADS, 0, s>>>(d, n, blk, clear);                       \
+    } while (0)
+    PS_DISPATCH_ONE(dtype, CALL);
+#undef CALL
+    return launch_rc();
+}
+
 // ---- fused exchange of shard totals over NVLink (mailboxes) --------------------------------
 int ps_publish_total(const void *total, void *const *peer_mailboxes, int n_peers, int rank, uint32_t epoch,
                      uint32_t prev_epoch, const void *own_mailbox, int *timeout_flag, void *stream) {

@@ -251,6 +251,26 @@ def scan_mailbox(x: torch.Tensor, out: torch.Tensor | None, mailbox_slots: int, 
     return total
 
 
+def tree_up_sweep(x: torch.Tensor) -> torch.Tensor:
+    """Blelloch up-sweep of a power-of-two span in place (element-typed,
+    simd.py:327-334); returns the root as a 1-element device tensor."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    root = torch.empty(1, dtype=x.dtype, device=x.device)
+    rc = _lib.load().ps_tree_up_sweep(_ptr(x), x.numel(), dtype_code(x.dtype), _ptr(root), _stream_ptr(x.device))
+    _lib.check(rc, "ps_tree_up_sweep")
+    return root
+
+
+def tree_down_sweep(x: torch.Tensor) -> None:
+    """Blelloch down-sweep of an up-swept power-of-two span in place
+    (simd.py:338-347): the span becomes its exclusive scan."""
+    _require_cuda(x, "x")
+    _flat(x, "x")
+    rc = _lib.load().ps_tree_down_sweep(_ptr(x), x.numel(), dtype_code(x.dtype), _stream_ptr(x.device))
+    _lib.check(rc, "ps_tree_down_sweep")
+
+
 class stall_injection:
     """Context manager: in-kernel stall injection for stress tests (the GPU form
     of the reference's ``ScanRequest.delay_hook``, engine.py:91).  Every role

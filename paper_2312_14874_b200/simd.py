@@ -16,7 +16,9 @@ checks, in/out-of-place behaviour and the exact returned totals:
   ps_reduce_batched, ps_add_offset_batched); vertical_scan is one scan.
 * tree family (simd.py:324-427): tree_scan / tree_scan_auto are one scan;
   their uint32 totals (root kept in the element dtype) are reproduced from
-  the scanned output at the peeled block boundaries.
+  the scanned output at the peeled block boundaries.  The step functions
+  up_sweep / down_sweep run the reference's exact Blelloch pairing on the
+  GPU (ps_tree_up_sweep / ps_tree_down_sweep).
 
 lane_shift_with_zero_fill / vector_inclusive_scan / AddRoundCounter describe
 the w-lane register primitive itself; they stay host-side numpy models of the
@@ -235,6 +237,30 @@ def _wrap_u32_total(total: int, offset) -> int:
     """offset + (span sum mod 2^32): the tree root is kept in a uint32 element."""
     off = int(coerce_offset(offset, np.uint32))
     return (off + ((int(total) - off) & 0xFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+
+
+def up_sweep(data, span: Span):
+    """Reduction sweep building the conceptual tree in place; returns the root
+    (simd.py:356-360).  Element-typed arithmetic in the reference's exact
+    pairing on the GPU (ps_tree_up_sweep), so float results are bit-identical."""
+    _check_buffer(data)
+    span.check(data)
+    _require_tree_length(span.len, 1)
+    v = DeviceView(data, span)
+    root = dev.tree_up_sweep(v.t)
+    v.commit()
+    return root.cpu().numpy()[0]
+
+
+def down_sweep(data, span: Span) -> None:
+    """Distribution sweep: turns an up-swept span into its exclusive scan
+    (simd.py:363-367), on the GPU (ps_tree_down_sweep)."""
+    _check_buffer(data)
+    span.check(data)
+    _require_tree_length(span.len, 1)
+    v = DeviceView(data, span)
+    dev.tree_down_sweep(v.t)
+    v.commit()
 
 
 def tree_scan(data, span: Span, offset=0, w: int = DEFAULT_LANE_WIDTH, scratch=None):
