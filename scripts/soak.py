@@ -1,0 +1,93 @@
+"""Randomised soak test of every scan path against numpy (dev tool):
+
+    python scripts/soak.py [seconds]
+
+Random dtype pairs, sizes (1 .. 2^27), unaligned views, inclusive/exclusive,
+seeds, forced kernels (look-back / L2 rounds / stream / auto), batched rows
+(both kernels), compaction, with and without stall injection.  Prints a line
+per 100 cases and exits non-zero on the first mismatch (with its parameters)."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2312_14874_b200 import _lib, device as dev  # noqa: E402
+
+lib = _lib.load()
+PAIRS = [(np.int32, np.int32), (np.int32, np.int64), (np.int64, np.int64), (np.uint32, np.uint64),
+         (np.uint32, np.uint32), (np.float32, np.float32), (np.float32, np.float64), (np.float64, np.float64)]
+rng = np.random.default_rng(int(time.time()))
+deadline = time.time() + (float(sys.argv[1]) if len(sys.argv) > 1 else 300)
+cases = 0
+
+
+def ref_scan(a, dout, exclusive, seed):
+    acc = np.float64 if np.dtype(dout).kind == "f" else (np.uint64 if np.dtype(a.dtype).kind == "u" else np.int64)
+    c = np.cumsum(a.astype(acc)) + acc(seed) if a.size else np.zeros(0, acc)
+    if exclusive and a.size:
+        c = np.concatenate([[acc(seed)], c[:-1]])
+    return c.astype(dout)
+
+
+def compare(got, want, what):
+    if np.dtype(want.dtype).kind == "f":
+        w = want.astype(np.float64)
+        rel = np.abs(got.astype(np.float64) - w) / np.maximum(np.abs(w), 1e-30)
+        ok = got.size == 0 or rel.max() <= 2e-6
+    else:
+        ok = np.array_equal(got, want)
+    if not ok:
+        raise SystemExit(f"MISMATCH {what}")
+
+
+while time.time() < deadline:
+    din, dout = PAIRS[rng.integers(len(PAIRS))]
+    n = int(rng.choice([1, 7, 4096, 8191, 100_003, 1 << 20, 3_000_001, 1 << 24, (1 << 25) + 17, 1 << 27]))
+    off = int(rng.integers(0, 8))
+    excl = bool(rng.integers(2))
+    seed = int(rng.integers(0, 50))
+    kern = int(rng.integers(0, 4))
+    stall = rng.random() < 0.15
+    if np.dtype(din).kind == "f":
+        a = rng.random(n + off).astype(din)
+    else:
+        a = rng.integers(0, 100, n + off).astype(din)
+    x = torch.from_numpy(a).cuda()[off:]
+    out = torch.empty(n, dtype=torch.from_numpy(np.zeros(1, dout)).dtype, device="cuda")
+    lib.ps_set_tuning(b"scan_kernel", kern)
+    try:
+        if stall:
+            with dev.stall_injection(seed=cases + 1, prob=0.1, max_ns=10000):
+                dev.scan(x, out, exclusive=excl, seed=seed)
+        else:
+            dev.scan(x, out, exclusive=excl, seed=seed)
+    finally:
+        lib.ps_set_tuning(b"scan_kernel", 0)
+    compare(out.cpu().numpy(), ref_scan(a[off:], dout, excl, seed),
+            f"scan {din.__name__}->{dout.__name__} n={n} off={off} excl={excl} seed={seed} kernel={kern} stall={stall}")
+    cases += 1
+    if cases % 7 == 0:  # batched rows
+        rows, cols = int(rng.integers(1, 700)), int(rng.integers(1, 40000))
+        b = rng.integers(0, 255, (rows, cols)).astype(np.int32)
+        lib.ps_set_tuning(b"rows_kernel", int(rng.integers(0, 3)))
+        o = torch.empty((rows, cols), dtype=torch.int64, device="cuda")
+        dev.scan_batched(torch.from_numpy(b).cuda(), o, exclusive=excl)
+        lib.ps_set_tuning(b"rows_kernel", 0)
+        want = np.cumsum(b, axis=1, dtype=np.int64)
+        if excl:
+            want = want - b
+        compare(o.cpu().numpy(), want, f"rows {rows}x{cols} excl={excl}")
+    if cases % 11 == 0:  # compaction
+        m = int(rng.choice([1000, 1 << 20, 5_000_000]))
+        v = rng.integers(-1000, 1000, m).astype(np.int32)
+        f = (rng.random(m) < rng.random()).astype(np.int32)
+        lib.ps_set_tuning(b"select_kernel", int(rng.integers(0, 3)))
+        o, cnt = dev.select(torch.from_numpy(v).cuda(), torch.from_numpy(f).cuda())
+        lib.ps_set_tuning(b"select_kernel", 0)
+        k = int(cnt.item())
+        compare(o[:k].cpu().numpy(), v[f != 0], f"select m={m}")
+    if cases % 100 == 0:
+        print(f"{cases} cases ok", flush=True)
+print(f"soak ok: {cases} cases")
