@@ -1,0 +1,110 @@
+// scripts/stream_variants.cu -- geometry sweep of scan_stream_kernel (smem-resident regions), dev tool.
+#include <cstdio>
+#include <cstdlib>
+#include "stream2_kernel.cuh"
+using namespace ps;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
+
+template <typename T>
+__global__ void fill_kernel(T *p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (T)(i % 3 + 1);
+}
+
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, int MINB = 1>
+void run_unused(const char *name, void *in, void *out, int64_t n, void *scratch, uint32_t &epoch, int64_t portion_bytes) {
+    using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
+    auto kern = scan_stream_kernel<TIn, TOut, SW, ROWS, NBUF, RWP, false, MINB>;
+    fill_kernel<TIn><<<1184, 256>>>((TIn *)in, n);
+    const int64_t unit = (int64_t)SW * Geo::CHUNK;
+    int64_t P = portion_bytes / (int64_t)sizeof(TIn) / unit * unit;
+    if (P < unit) P = unit;
+    if (P > (int64_t)Geo::MAXC * Geo::CHUNK) P = (int64_t)Geo::MAXC * Geo::CHUNK / unit * unit;
+    const int smem = Geo::smem(P);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+        printf("%s: smem %d too large\n", name, smem);
+        cudaGetLastError();
+        return;
+    }
+    int per = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, Geo::THREADS, smem));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int64_t G = getenv("GRID") ? atoll(getenv("GRID")) : (int64_t)per * sms;
+    StreamArgs a{};
+    a.in = in; a.out = out; a.lo = 0; a.hi = n; a.portion = P;
+    a.rounds = (n + P * G - 1) / (P * G);
+    a.desc = (ulonglong2 *)((char *)scratch + 256);
+    void *params[] = {&a};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    const bool coop = getenv("NOCOOP") == nullptr;
+    for (int it = 0; it < 12; ++it) {
+        a.epoch = ++epoch;
+        cudaEventRecord(e0);
+        if (coop) CK(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(Geo::THREADS), params, smem, 0));
+        else kern<<<G, Geo::THREADS, smem>>>(a);
+        cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (it >= 2 && ms < best) best = ms;
+    }
+    int bad = 0;
+    for (int64_t i : {(int64_t)0, (int64_t)1, (int64_t)12345, n / 3, n / 2 + 7, n - 2, n - 1}) {
+        TOut got; CK(cudaMemcpy(&got, (TOut *)out + i, sizeof(TOut), cudaMemcpyDeviceToHost));
+        const int64_t m = i + 1, want = (m / 3) * 3 + (m % 3 == 2 ? 1 : 0) + m;
+        if ((double)got != (double)(TOut)want) ++bad;
+    }
+    printf("%-16s G=%lld P=%lld (%lld KB) rounds=%lld smem=%d: %.1f us  %.1f GB/s  %s\n", name, (long long)G,
+           (long long)P, (long long)(P * sizeof(TIn) >> 10), (long long)a.rounds, smem, best * 1e3,
+           (double)n * (sizeof(TIn) + sizeof(TOut)) / (best * 1e-3) / 1e9, bad ? "FAIL" : "ok");
+}
+
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int NG>
+void run2(const char *name, void *in, void *out, int64_t n, void *scratch, uint32_t &epoch) {
+    using Geo = Stream2Geom<TIn, TOut, SW, ROWS, NBUF, NG>;
+    auto kern = scan_stream2_kernel<TIn, TOut, SW, ROWS, NBUF, NG>;
+    fill_kernel<TIn><<<1184, 256>>>((TIn *)in, n);
+    const int64_t P = (int64_t)SW * Geo::CHUNK;
+    const int smem = Geo::smem(P);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t G = 148;
+    StreamArgs a{};
+    a.in = in; a.out = out; a.lo = 0; a.hi = n; a.portion = P;
+    a.rounds = (n + P * G - 1) / (P * G);
+    a.desc = (ulonglong2 *)((char *)scratch + 256);
+    void *params[] = {&a};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int it = 0; it < 12; ++it) {
+        a.epoch = ++epoch;
+        cudaEventRecord(e0);
+        CK(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(Geo::THREADS), params, smem, 0));
+        cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (it >= 2 && ms < best) best = ms;
+    }
+    int bad = 0;
+    for (int64_t i : {(int64_t)0, (int64_t)1, (int64_t)12345, n / 3, n / 2 + 7, n - 2, n - 1}) {
+        TOut got; CK(cudaMemcpy(&got, (TOut *)out + i, sizeof(TOut), cudaMemcpyDeviceToHost));
+        const int64_t m = i + 1, want = (m / 3) * 3 + (m % 3 == 2 ? 1 : 0) + m;
+        if ((double)got != (double)(TOut)want) ++bad;
+    }
+    printf("%-16s P=%lld (%lld KB) smem=%d: %.1f us  %.1f GB/s  %s\n", name, (long long)P,
+           (long long)(P * sizeof(TIn) >> 10), smem, best * 1e3,
+           (double)n * (sizeof(TIn) + sizeof(TOut)) / (best * 1e-3) / 1e9, bad ? "FAIL" : "ok");
+}
+
+int main() {
+    void *in, *out, *scratch;
+    CK(cudaMalloc(&in, 1ll << 32)); CK(cudaMalloc(&out, 1ll << 32)); CK(cudaMalloc(&scratch, 64 << 20));
+    CK(cudaMemset(scratch, 0, 64 << 20));
+    uint32_t epoch = 0;
+    const int64_t N = 1ll << 28;
+    run2<float, float, 8, 4, 6, 2>("s2 f32 8x2g nb6", in, out, N, scratch, epoch);
+    run2<float, float, 6, 4, 6, 2>("s2 f32 6x2g nb6", in, out, N, scratch, epoch);
+    run2<float, float, 8, 2, 6, 2>("s2 f32 8x2g r2", in, out, N, scratch, epoch);
+    run2<float, float, 4, 4, 12, 3>("s2 f32 4x3g nb12", in, out, N, scratch, epoch);
+    run2<int64_t, int64_t, 8, 4, 6, 2>("s2 i64 8x2g", in, out, N, scratch, epoch);
+    run2<int, int64_t, 8, 4, 6, 2>("s2 i32 8x2g", in, out, N, scratch, epoch);
+    run2<int64_t, int64_t, 8, 4, 6, 2>("s2 i64 2^24", in, out, 1ll << 24, scratch, epoch);
+    return 0;
+}
