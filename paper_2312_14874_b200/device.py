@@ -473,7 +473,7 @@ def _host_pointer(a) -> tuple[int, int, int]:
 
 def scan_host(x, out=None, *, exclusive: bool = False, seed=0, chunk_elems: int | None = None,
               device: torch.device | int | None = None):
-    """Scan HOST memory end to end (H2D -> look-back scan -> D2H, pipelined in
+    """Scan HOST memory end to end (H2D -> scan -> D2H, pipelined in
     chunks over three streams).  ``out`` defaults to ``x`` (in place).  Pinned
     host memory gives full PCIe overlap; pageable memory works but serialises.
     Blocks; returns the accumulator-precision total as a Python number."""

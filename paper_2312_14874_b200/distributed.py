@@ -11,7 +11,7 @@ plan.py:160-178) mapped onto the GPUs of one box:
     (engine.py:329-331) becomes ``carry_g = seed + sum(totals[:g])``,
     evaluated *on the device* by the consuming kernel (seed_terms), so no
     host round trip sits between the passes;
-  * pass 2: a carry-in look-back scan.
+  * pass 2: a carry-in scan (the same 1-D kernel, seeded on the device).
 
 Two schemes, named as in plan.py:24-37:
   ACCUMULATE_SCAN_EQUAL  reduce-then-scan: read n/G, exchange, read+write n/G

@@ -6,11 +6,13 @@ threads: pass 1 (local scans or partition totals) -> one barrier -> pass 2
 double-buffered ledger (engine.py:278-344).
 
 On one B200 that whole structure is the *inside* of a single kernel launch:
-each 8-warp CTA is a "partition", its pass 1 is the in-register tile
-reduction, the barrier + ledger fold is the decoupled look-back over the
-predecessors' published aggregates, and pass 2 is the store of the carried
-tile -- one read and one write per element, every scheme collapsing to the
-same single pass.  Across GPUs the two passes are real again (see
+each persistent CTA's portion of a region is a "partition" held in shared
+memory, its pass 1 is the reducer warps' chunk totals, the barrier + ledger
+fold is the grid-wide gather of the portion totals (fixed order, so float
+carries are identical on every CTA), and pass 2 is the scanner warps'
+carried scan of the same shared-memory copy -- one HBM read and one write per
+element, every scheme collapsing to the same single launch (stream_kernel.cuh;
+small inputs use the decoupled look-back kernel).  Across GPUs the two passes are real again (see
 ``distributed.py``): there SchemeId selects reduce-then-scan or
 scan-then-fixup.
 
@@ -143,8 +145,8 @@ class RunStats:
 class ScanEngine:
     """One scan at a time per engine (engine.py:149-155); executes requests
     on the current CUDA device through ``core.scan_into`` (one launch of the
-    library's 1-D scan: the L2-region accumulate-scan kernel for large
-    inputs, the decoupled look-back kernel otherwise)."""
+    library's 1-D scan: the shared-memory-region accumulate-scan kernel for
+    large inputs, the decoupled look-back kernel otherwise)."""
 
     def __init__(self, threads: int = 1, affinity: str = "none"):
         if threads < 1:

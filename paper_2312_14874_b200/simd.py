@@ -1,9 +1,9 @@
 """Drop-in for ``prefixscan.simd`` (reference: pkg/src/prefixscan/simd.py).
 
 The reference models three CPU SIMD kernel families over a w-lane register
-(w in {4, 8, 16}).  On the B200 the "register" is a 32-lane warp and a tile
-of 8 warps, so every family's *result* comes from the same look-back scan
-kernel; what is kept per family is its public contract -- names, argument
+(w in {4, 8, 16}).  On the B200 the "register" is a 32-lane warp and a chunk
+of rows per warp, so every family's *result* comes from the same 1-D scan
+launch (ps_scan); what is kept per family is its public contract -- names, argument
 checks, in/out-of-place behaviour and the exact returned totals:
 
 * horizontal_scan (simd.py:134-148): for uint32 data the reference carries
