@@ -84,3 +84,15 @@ def test_public_entry_matches_reference(mod, name, desc):
         ours = list(inspect.signature(getattr(obj, meth)).parameters)
         extra = EXTRA_PARAMS.get((mod, name), set())
         assert [p for p in ours if p not in extra][:len(params)] == params, f"{mod}.{name}.{meth}{ours}"
+
+
+def test_install_as_prefixscan_aliases_every_module():
+    import subprocess
+    import sys
+    code = ("import paper_2312_14874_b200 as b; b.install_as_prefixscan(); "
+            "import prefixscan, prefixscan.core as c, prefixscan.simd as s; "
+            "from prefixscan.engine import ScanRequest; from prefixscan.bench import run_case; "
+            "assert prefixscan is b and c.__name__ == 'paper_2312_14874_b200.core'; print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         cwd=os.path.dirname(HERE))
+    assert out.stdout.strip() == "ok", out.stderr
