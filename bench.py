@@ -339,14 +339,13 @@ def run_ours(args, cfg, cfg_name):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # events only around the K steps: an event recorded between two cooperative
+    # launches delays the next one by ~3 us (scripts/launch_gap.py)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         t_start.record(stream)
-        for k in range(args.steps):
-            ev[k][0].record(stream)
+        for _ in range(args.steps):
             step()
-            ev[k][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -355,7 +354,6 @@ def run_ours(args, cfg, cfg_name):
         if getattr(sharded, "mailbox", None) is not None:
             sharded.mailbox.check()  # a fused-exchange wait that gave up invalidates the run
     elapsed_ms = t_start.elapsed_time(t_end)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
     if world > 1:
         tt = torch.tensor([elapsed_ms], device=dev_t)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -363,9 +361,10 @@ def run_ours(args, cfg, cfg_name):
     total_elems = n * world
     value = total_elems * args.steps / (elapsed_ms / 1e3)
 
-    # dominant kernel: the scan (per-launch CUDA events; at N>1 the step's events
-    # also bracket the reduce + all-gather, so use the scan-only loop below)
-    kernel_ms = statistics.mean(step_ms)
+    # dominant kernel: the scan.  At N=1 a step is one scan launch, so its average
+    # launch duration is the timed region / K (launch gaps included); at N>1 a step
+    # also holds the reduce + exchange, so the scan-only loop below times it
+    kernel_ms = elapsed_ms / args.steps
     if world > 1 or args.force_sharded:
         kernel_ms = _scan_kernel_ms(device, x, out, exclusive, rows, stream, args.steps)
     esize_in = x.element_size()
@@ -394,7 +393,8 @@ def run_ours(args, cfg, cfg_name):
             "config": {"workload": cfg["desc"], "elements_per_gpu": n,
                        "parallelism": (f"{world} GPU(s), contiguous shards, {scheme.value}, exchange {exchange}"
                                        if world > 1 or args.force_sharded else "1 GPU"),
-                       "l2": "no flush: in+out per step >= 1 GiB >> 126 MB L2"},
+                       "l2": (f"no flush: input {n * esize_in / 1e6:.0f} MB + output {n * esize_out / 1e6:.0f} MB "
+                              f"per step and GPU > 126 MB L2")},
             "achieved_gbs": achieved, "hbm_frac_measured": achieved / peak,
             "hbm_frac_nominal": achieved / NOMINAL_HBM_GBS,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -469,13 +469,13 @@ def _device_input(cfg, g, dev_t, tdt):
 def _scan_kernel_ms(device, x, out, exclusive, rows, stream, steps):
     import torch
     reps = max(5, min(steps, 50))
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-    for a, b in ev:
-        a.record(stream)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
         device.scan(x, out, exclusive=exclusive)
-        b.record(stream)
+    b.record(stream)
     torch.cuda.synchronize()
-    return statistics.mean(a.elapsed_time(b) for a, b in ev)
+    return a.elapsed_time(b) / reps
 
 
 def _verify(cfg, x_host, out):
