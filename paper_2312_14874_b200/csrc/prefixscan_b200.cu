@@ -83,6 +83,7 @@ struct Tuning {
     int64_t round_ramp = 0;                 // ramp regions at each end (sizes P/2^k .. P/2); 0 = off
     int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)
     int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
+    int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
 };
 Tuning g_tune;
@@ -269,6 +270,7 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     a.desc = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
     a.epoch = epoch;
     a.exclusive = exclusive;
+    a.inflight = g_tune.stream_inflight;
     void *params[] = {&a};
     const void *kern = (const void *)SKERN;
     if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
@@ -619,6 +621,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "rows_kernel")) {
         if (value < 0 || value > 2) return PS_ERR_ARG;
         g_tune.rows_kernel = (int)value;
+    } else if (!std::strcmp(key, "stream_inflight")) {
+        if (value < 0 || value > 8) return PS_ERR_ARG;
+        g_tune.stream_inflight = (int)value;
     } else if (!std::strcmp(key, "select_kernel")) {
         if (value < 0 || value > 2) return PS_ERR_ARG;
         g_select_kernel = (int)value;
@@ -656,6 +661,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "round_prefetch")) return g_tune.round_prefetch;
     if (!std::strcmp(key, "rows_kernel")) return g_tune.rows_kernel;
     if (!std::strcmp(key, "select_kernel")) return g_select_kernel;
+    if (!std::strcmp(key, "stream_inflight")) return g_tune.stream_inflight;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;

@@ -40,6 +40,7 @@ struct StreamArgs {
     ulonglong2 *desc;  // rounds * G descriptors
     uint32_t epoch;
     int exclusive;
+    int inflight;      // producer: at most this many regions' loads outstanding (0: NBUF)
     Stall stall;       // stress tests: stall injection at every role hand-off
     Mailbox mail;      // seed += totals published by the ranks before this one
 };
@@ -130,6 +131,11 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                 const int b = (int)(r % NBUF);
                 stall_site<STALL>(a.stall, r * G + c, 0, 1);
                 if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
+                // bounded loads in flight: an SM's ledger polls return behind its own
+                // outstanding TMA data, so six regions issued at start-up would hold
+                // the first grid-wide gather back by ~5 us
+                if (r >= a.inflight && a.inflight > 0 && a.inflight < NBUF)
+                    mbar_wait(&full[(r - a.inflight) % NBUF], par(r - a.inflight));
 #ifdef PS_TRACE
                 if (g_trace && true) g_trace[(r * G + c) * 8 + 0] = gtimer();
 #endif

@@ -34,17 +34,21 @@ void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32
     a.in = in; a.out = out; a.lo = 0; a.hi = n; a.portion = P;
     a.rounds = (n + P * G - 1) / (P * G);
     a.desc = (ulonglong2 *)((char *)scratch + 256);
+    a.inflight = getenv("INFL") ? atoi(getenv("INFL")) : 0;
     void *params[] = {&a};
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e30f;
     const bool coop = getenv("NOCOOP") == nullptr;
-    for (int it = 0; it < 12; ++it) {
-        a.epoch = ++epoch;
+    for (int it = 0; it < 12; ++it) {  // best of 10 batches of 10 back-to-back launches
         cudaEventRecord(e0);
-        if (coop) CK(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(Geo::THREADS), params, smem, 0));
-        else kern<<<G, Geo::THREADS, smem>>>(a);
+        for (int k = 0; k < 10; ++k) {
+            a.epoch = ++epoch;
+            if (coop) CK(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(Geo::THREADS), params, smem, 0));
+            else kern<<<G, Geo::THREADS, smem>>>(a);
+        }
         cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 10;
         if (it >= 2 && ms < best) best = ms;
     }
     int bad = 0;
@@ -65,7 +69,20 @@ int main() {
     uint32_t epoch = 0;
     const int64_t N = 1ll << 28;
     const int64_t S = 1ll << 24;
+    if (getenv("MID")) {  // mid-size inputs, where start-up and drain matter
+        run<int64_t, int64_t, 8, 4, 6, 4>("i64_22", in, out, S / 4, scratch, epoch, 32 << 10);
+        run<int64_t, int64_t, 8, 4, 6, 4>("i64_23", in, out, S / 2, scratch, epoch, 32 << 10);
+        run<int64_t, int64_t, 8, 4, 6, 4>("i64_24", in, out, S, scratch, epoch, 32 << 10);
+        run<int64_t, int64_t, 8, 4, 6, 4>("i64_25", in, out, S * 2, scratch, epoch, 32 << 10);
+        run<float, float, 8, 4, 6, 4>("f32_23", in, out, S / 2, scratch, epoch, 32 << 10);
+        run<float, float, 8, 4, 6, 4>("f32_24", in, out, S, scratch, epoch, 32 << 10);
+        run<float, float, 8, 4, 6, 4>("f32_26", in, out, S * 4, scratch, epoch, 32 << 10);
+        return 0;
+    }
     run<float, float, 8, 4, 6, 4>("f32_28", in, out, N, scratch, epoch, 32 << 10);
-    run<float, float, 8, 4, 6, 4>("f32_28_again", in, out, N, scratch, epoch, 32 << 10);
+    run<int64_t, int64_t, 8, 4, 6, 4>("i64_24", in, out, S, scratch, epoch, 32 << 10);
+    run<int64_t, int64_t, 8, 4, 6, 4>("i64_27", in, out, N / 2, scratch, epoch, 32 << 10);
+    run<int32_t, int64_t, 8, 4, 6, 4>("i32_i64_28", in, out, N, scratch, epoch, 32 << 10);
+    run<float, float, 8, 4, 6, 4>("f32_24", in, out, S, scratch, epoch, 32 << 10);
     return 0;
 }

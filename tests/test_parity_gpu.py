@@ -261,6 +261,26 @@ def test_both_scan_kernels(ps, force_kernel, kernel, dt):
                     assert int(tv.item()) == int(xs.astype(np.int64).sum()) + 5, ctx
 
 
+@pytest.mark.parametrize("inflight", [0, 1, 2, 5])
+def test_stream_kernel_inflight_limit(ps, force_kernel, inflight):
+    """The producer's bound on outstanding region loads changes only timing."""
+    from paper_2312_14874_b200 import _lib, device
+    lib = _lib.load()
+    prev = lib.ps_get_tuning(b"stream_inflight")
+    force_kernel(3)
+    assert lib.ps_set_tuning(b"stream_inflight", inflight) == 0
+    try:
+        r = np.random.default_rng(31)
+        for dt, n in ((np.int64, 7_000_003), (np.float32, 9_000_011), (np.int32, 1 << 22)):
+            x = GENS[dt](r, n)
+            t = _cuda(x)
+            o = torch.empty(n, dtype=torch.int64 if dt == np.int32 else t.dtype, device="cuda")
+            device.scan(t, o, exclusive=dt == np.int32)
+            _assert_array(_host(o), _expected(x, 0, dt == np.int32, np.int64 if dt == np.int32 else None), f"inflight={inflight} {dt.__name__}")
+    finally:
+        lib.ps_set_tuning(b"stream_inflight", prev)
+
+
 @pytest.mark.parametrize("kernel", [2, 3])
 def test_rounds_kernel_widening_and_chaining(ps, force_kernel, kernel):
     from paper_2312_14874_b200 import device
