@@ -251,7 +251,8 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "rounds_min_bytes" auto mode uses the shared-memory-region (stream) kernel from
  *                      this input size (smaller inputs: the look-back kernel)
  *   "select_kernel"    ps_select: 0 = auto, 1 = three launches, 2 = single pass (compaction)
- *   "stream_inflight"  stream kernel: at most this many regions' loads outstanding per SM
+ *   "stream_inflight"  stream scan and single-pass select kernels: at most this many
+ *                      regions' loads outstanding per SM
  *                      (default 2; 0 = as many as the buffer ring holds)
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,

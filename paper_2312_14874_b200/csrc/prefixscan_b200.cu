@@ -562,6 +562,7 @@ int launch_select_stream(const void *values, const void *flags, int64_t n, void 
     a.desc = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
     // the high word makes a stale count (a small integer) in this scratch unmistakable for a tag
     a.want = ((uint64_t)(~epoch) << 32) | ((uint64_t)epoch << 2);
+    a.inflight = g_tune.stream_inflight;
     void *params[] = {&a};
     return cuda_rc(cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)G), dim3(SS_THREADS), params,
                                                Geo::SMEM, s));

@@ -28,6 +28,7 @@ struct SelectArgs {
     long long *count;  // total selected (device, nullable)
     ulonglong2 *desc;  // rounds * G descriptors
     uint64_t want;     // descriptor tag: (~epoch << 32) | (epoch << 2) -- never matches a small count
+    int inflight;      // producer: at most this many regions' loads outstanding (0: NBUF)
 };
 
 constexpr int SS_SW = 8, SS_RWP = 4, SS_ROWS = 2, SS_VEC = 8;
@@ -121,6 +122,8 @@ __global__ void __launch_bounds__(SS_THREADS, 1) select_stream_kernel(const Sele
             for (int64_t r = 0; r < a.rounds; ++r) {
                 const int b = (int)(r % NBUF);
                 if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
+                if (r >= a.inflight && a.inflight > 0 && a.inflight < NBUF)  // see scan_stream_kernel
+                    mbar_wait(&full[(r - a.inflight) % NBUF], par(r - a.inflight));
                 const int64_t p0 = p0_of(r);
                 if (p0 + P <= a.n) {
                     mbar_expect_tx(&full[b], Geo::BUF);

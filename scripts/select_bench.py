@@ -6,7 +6,13 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
+import os  # noqa: E402
+
+from paper_2312_14874_b200 import _lib  # noqa: E402
 from paper_2312_14874_b200 import device as dev  # noqa: E402
+
+if os.environ.get("INFL"):  # the single-pass kernel's bound on outstanding region loads
+    _lib.load().ps_set_tuning(b"stream_inflight", int(os.environ["INFL"]))
 
 n = 1 << 28
 g = torch.Generator(device="cuda").manual_seed(5)
