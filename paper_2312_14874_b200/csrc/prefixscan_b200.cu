@@ -221,6 +221,8 @@ constexpr int SSW = 8, SROWS = 4, SNBUF = 6, SRWP = 4;
 #define SKERN scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP>
 #define SKERN_STALL scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP, true>
 
+constexpr int STREAM_MAX_GRID = 32 * GATHER_LP;  // the ledger warp gathers <= 5 descriptors per lane
+
 template <typename TIn, typename TOut>
 int64_t stream_portion() {  // positions per CTA per region: NBUF buffers in ~200 KB
     constexpr int64_t unit = (int64_t)SSW * SGEO::CHUNK;
@@ -250,7 +252,7 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
                   const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
                   uint32_t epoch, cudaStream_t s, const Mailbox *mail = nullptr) {
     const int64_t G = stream_grid<TIn, TOut>();
-    if (G <= 0 || G > 256) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
+    if (G <= 0 || G > STREAM_MAX_GRID) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
     const int64_t P = stream_portion<TIn, TOut>();
     const int64_t rounds = (lead + n + P * G - 1) / (P * G);
     if (!scratch || scratch_bytes < 256 + (size_t)(rounds * G) * 16) return PS_ERR_SCRATCH;
@@ -375,7 +377,8 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     a.vec_ok = vec;
     a.lead = vec ? lead : 0;
     const bool big = cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes;
-    if (rows == 1 && vec && (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big)))
+    if (rows == 1 && vec &&
+        (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big && stream_grid<TIn, TOut>() <= STREAM_MAX_GRID)))
         return launch_stream<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
                                         scratch, scratch_bytes, epoch, s, mail);
     if (rows == 1 && vec && g_tune.scan_kernel == 2)

@@ -72,6 +72,44 @@ __device__ __forceinline__ void widen_chunk(const V256 (&raw)[ROWS], A (&v)[ROWS
     }
 }
 
+// Ledger gather with its round trip overlapped.  One grid-wide gather of a
+// region's G descriptors is one L2 round trip (~1-1.3 us under full HBM load,
+// scripts/trace_stream.cu), and the ledger warp's per-region chain -- gather,
+// fold, hand-off -- sets the kernel's region rate whenever the reducers run
+// ahead of it.  So the loads of region r+1 are issued as soon as region r's have
+// arrived (the totals are normally published by then) and the chunk-total scan,
+// which needs only this CTA's reducers, runs while they are in flight: the
+// chain per region is one round trip (integer data; see the ledger for float32).
+// Issuing gathers further ahead was slower: polls that return before the totals
+// are published cost a full extra round trip each (measured 8-25 % slower at
+// 2-3 regions ahead).
+constexpr int GATHER_LP = 5;  // descriptors per lane: the stream kernel runs with G <= 160 CTAs
+
+__device__ __forceinline__ void desc_issue(ulonglong2 (&d)[GATHER_LP], const ulonglong2 *base, int G, int lane) {
+#pragma unroll
+    for (int i = 0; i < GATHER_LP; ++i)
+        if (lane + 32 * i < G) d[i] = ld_desc(base + lane + 32 * i);
+}
+
+// poll until every descriptor of the region carries this launch's tag
+__device__ __forceinline__ void desc_wait(ulonglong2 (&d)[GATHER_LP], const ulonglong2 *base, int G, uint64_t want,
+                                          int lane) {
+    unsigned pending = 0;
+#pragma unroll
+    for (int i = 0; i < GATHER_LP; ++i)
+        if (lane + 32 * i < G) pending |= 1u << i;
+    while (true) {
+#pragma unroll
+        for (int i = 0; i < GATHER_LP; ++i)
+            if (((pending >> i) & 1) && (d[i].x & ~3ull) == want && (d[i].x & 3ull) != 0) pending &= ~(1u << i);
+        if (!__any_sync(FULL, pending != 0)) break;
+        __nanosleep(32);
+#pragma unroll
+        for (int i = 0; i < GATHER_LP; ++i)
+            if ((pending >> i) & 1) d[i] = ld_desc(base + lane + 32 * i);
+    }
+}
+
 template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, bool STALL = false, int MINB = 1>
 __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(const StreamArgs a) {
     using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
@@ -225,37 +263,60 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
             if (a.mail.n) carry += mailbox_sum<A>(a.mail, lane);
         }
+        // integer data: next gather issued early and the chunk scan inside the round trip
+        // (int64 2^27 -2 %, cfg1 unchanged); float32: gathers issued on their own turn
+        // (the early poll made cfg2 2.6 % slower: its reducers, not the ledger, set the pace)
+        constexpr bool OVERLAP = !FLOAT;
+        ulonglong2 dn[GATHER_LP];  // the gather in flight (launcher: G <= 32 * GATHER_LP)
+        if (OVERLAP) desc_issue(dn, a.desc, G, lane);
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
-            A sb, sa;
             stall_site<STALL>(a.stall, r * G + c, 0, 4);
-#ifdef PS_EXP_NOLEDGER
-            sb = sa = (A)0;
-#else
+            const A *tot = chunk_tot + b * MAXC;
+            A *pr = chunk_pre + b * MAXC;
+            A ex = (A)0, t0 = (A)0;
+            auto chunk_prefix = [&]() {  // exclusive scan of this portion's chunk totals
+                mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
+                // nchunk <= 64: two chunks per lane, exclusive scan across the warp
+                t0 = lane * 2 < nchunk ? tot[lane * 2] : (A)0;
+                const A t1 = lane * 2 + 1 < nchunk ? tot[lane * 2 + 1] : (A)0;
+                A incl = t0 + t1;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const A y = shfl_up(incl, dd);
+                    if (lane >= dd) incl += y;
+                }
+                ex = shfl_up(incl, 1);
+                if (lane == 0) ex = (A)0;
+            };
+            if (OVERLAP) chunk_prefix();
+            A sb = (A)0, sa = (A)0;
+#ifndef PS_EXP_NOLEDGER
 #ifdef PS_TRACE
             if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 3] = gtimer();
 #endif
-            gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
-#ifdef PS_TRACE
-                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
-#endif
-#endif
-
-            mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
-            const A *tot = chunk_tot + b * MAXC;
-            A *pr = chunk_pre + b * MAXC;
-            // nchunk <= 64: two chunks per lane, exclusive scan across the warp
-            const A t0 = lane * 2 < nchunk ? tot[lane * 2] : (A)0;
-            const A t1 = lane * 2 + 1 < nchunk ? tot[lane * 2 + 1] : (A)0;
-            const A own = t0 + t1;
-            A incl = own;
+            if (!OVERLAP) desc_issue(dn, a.desc + r * G, G, lane);
+            desc_wait(dn, a.desc + r * G, G, want, lane);
 #pragma unroll
-            for (int dd = 1; dd < 32; dd <<= 1) {
-                const A y = shfl_up(incl, dd);
-                if (lane >= dd) incl += y;
+            for (int i = 0; i < GATHER_LP; ++i) {  // gather_totals' summation order
+                const int j = lane + 32 * i;
+                if (j < G) {
+                    const A v = acc_from_bits<A>(dn[i].y);
+                    sa += v;
+                    if (j < c) sb += v;
+                }
             }
-            A ex = shfl_up(incl, 1);
-            if (lane == 0) ex = (A)0;
+            if (OVERLAP && r + 1 < a.rounds) desc_issue(dn, a.desc + (r + 1) * G, G, lane);
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {  // both warp sums in one pass
+                sa += __shfl_xor_sync(FULL, sa, d);
+                sb += __shfl_xor_sync(FULL, sb, d);
+            }
+#ifdef PS_TRACE
+            if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
+#endif
+#endif
+            if (!OVERLAP) chunk_prefix();
             const A base = carry + sb + ex;
             if (lane * 2 < nchunk) pr[lane * 2] = base;
             if (lane * 2 + 1 < nchunk) pr[lane * 2 + 1] = base + t0;
@@ -264,7 +325,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             __syncwarp();
             if (lane == 0) mbar_arrive(&pre[b]);
 #ifdef PS_TRACE
-                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
+            if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
 #endif
         }
         if (c == 0 && lane == 0 && a.total) *reinterpret_cast<A *>(a.total) = carry;

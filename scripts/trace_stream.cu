@@ -23,7 +23,7 @@ void run(const char *name, void *in, void *out, int64_t n, void *scratch, uint32
     a.in = in; a.out = out; a.lo = 0; a.hi = n; a.portion = P;
     a.rounds = (n + P * G - 1) / (P * G);
     a.desc = (ulonglong2 *)((char *)scratch + 256);
-    a.inflight = getenv("INFL") ? atoi(getenv("INFL")) : 0;
+    a.inflight = getenv("INFL") ? atoi(getenv("INFL")) : 2;
     void *params[] = {&a};
     for (int w = 0; w < 3; ++w) { a.epoch = ++epoch; CK(cudaLaunchCooperativeKernel((const void *)kern, dim3(G), dim3(Geo::THREADS), params, smem, 0)); }
     CK(cudaDeviceSynchronize());
