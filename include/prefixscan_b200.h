@@ -34,7 +34,9 @@
  *   ZERO-FILLED when first allocated, and each launch on one scratch buffer
  *   needs a fresh `epoch` in [1, PS_EPOCH_MAX] strictly greater than the
  *   previous one (descriptors are epoch-tagged, so no per-call memset).  When
- *   the epochs run out, zero the buffer again and restart at 1.
+ *   the epochs run out, zero the buffer again and restart at 1.  (The first
+ *   16 bytes of a batched scan's scratch are the rows kernel's row ticket;
+ *   every launch leaves them at zero again.)
  * - `in == out` (in place) is allowed; partial overlap is not.
  * - Return 0 on success, a PS_ERR_* (>0) on misuse, or a cudaError_t value
  *   offset by PS_ERR_CUDA_BASE on a CUDA failure.
@@ -254,6 +256,9 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "stream_inflight"  stream scan and single-pass select kernels: at most this many
  *                      regions' loads outstanding per SM
  *                      (default 2; 0 = as many as the buffer ring holds)
+ *   "rows_dynamic"     rows kernel: 1 = rows handed out from a grid-wide ticket kept in
+ *                      the scratch's control words (faster SMs take more rows),
+ *                      0 = CTA c takes rows c, c+G, ... (default 1)
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability

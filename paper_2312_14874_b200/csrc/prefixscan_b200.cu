@@ -84,6 +84,7 @@ struct Tuning {
     int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)
     int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
     int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
+    int rows_dynamic = 1;                   // rows kernel: rows from a grid-wide ticket (0 = fixed shares)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
 };
 Tuning g_tune;
@@ -320,8 +321,10 @@ bool rows_kernel_applies(const void *in, int64_t rows, int64_t cols, int64_t ld_
 
 template <typename TIn, typename TOut>
 int launch_rows(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int exclusive,
-                const void *row_seeds, void *row_totals, cudaStream_t s) {
+                const void *row_seeds, void *row_totals, void *scratch, size_t scratch_bytes, cudaStream_t s) {
     RowsArgs a{};
+    // rows from a grid-wide ticket in the scratch's control words (zero between launches)
+    if (g_tune.rows_dynamic && scratch && scratch_bytes >= 256) a.ctr = static_cast<unsigned long long *>(scratch);
     a.stall = g_tune.stall;
     a.in = in;
     a.out = out;
@@ -628,6 +631,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "stream_inflight")) {
         if (value < 0 || value > 8) return PS_ERR_ARG;
         g_tune.stream_inflight = (int)value;
+    } else if (!std::strcmp(key, "rows_dynamic")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.rows_dynamic = (int)value;
     } else if (!std::strcmp(key, "select_kernel")) {
         if (value < 0 || value > 2) return PS_ERR_ARG;
         g_select_kernel = (int)value;
@@ -666,6 +672,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "rows_kernel")) return g_tune.rows_kernel;
     if (!std::strcmp(key, "select_kernel")) return g_select_kernel;
     if (!std::strcmp(key, "stream_inflight")) return g_tune.stream_inflight;
+    if (!std::strcmp(key, "rows_dynamic")) return g_tune.rows_dynamic;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;
@@ -710,7 +717,8 @@ int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64
     if (rows == 1) ld_in = ld_out = cols;
 #define CALL(TI, TO)                                                                                            \
     if (rows > 1 && rows_kernel_applies<TI, TO>(in, rows, cols, ld_in))                                         \
-        return launch_rows<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, row_seeds, row_totals, s);   \
+        return launch_rows<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, row_seeds, row_totals, scratch, \
+                                   scratch_bytes, s);                                                           \
     return launch_scan<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, 0, row_seeds, row_seeds ? rows : 0, \
                                row_totals, scratch, scratch_bytes, epoch, s)
     PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);

@@ -27,6 +27,8 @@ struct RowsArgs {
     void *row_totals;                   // acc-typed, nullable
     int exclusive;
     int vec_out;                        // output rows are 32-byte aligned
+    unsigned long long *ctr;            // [row ticket, producers done], zero between launches;
+                                        // null: CTA c takes rows c, c + G, ...
     Stall stall;                        // stress tests: stall injection
 };
 
@@ -38,7 +40,7 @@ struct RowsGeom {
     static constexpr int CHUNK = RPC * ROW_ELEMS;  // elements per chunk (RPC KiB)
     static constexpr int SEG = NCH * CHUNK;        // elements per work item
     static constexpr int SEG_BYTES = SEG * (int)sizeof(TIn);
-    static constexpr int SMEM = NBUF * SEG_BYTES + 2 * NBUF * 8 + NBUF * NCH * 8 + 64;
+    static constexpr int SMEM = NBUF * SEG_BYTES + 2 * NBUF * 8 + NBUF * NCH * 8 + NBUF * 16 + 64;
 };
 
 template <typename TIn, typename TOut, int SW, int RPC, int NBUF, int NCH, bool STALL = false>
@@ -55,6 +57,8 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)NBUF * Geo::SEG_BYTES);
     uint64_t *freeb = full + NBUF;
     A *tot = reinterpret_cast<A *>(freeb + NBUF);  // [NBUF][NCH]
+    int64_t *item_row = reinterpret_cast<int64_t *>(tot + NBUF * NCH);  // [NBUF]: row of the item (-1: end)
+    int64_t *item_seg = item_row + NBUF;                                 // [NBUF]: its segment
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t G = gridDim.x, c = blockIdx.x;
@@ -73,14 +77,28 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
 
     if (warp == SW) {
         // =========================== producer ======================================
+        // Rows are taken from a grid-wide ticket when a.ctr is given: an SM that
+        // streams faster takes more rows (fixed shares leave the grid waiting for the
+        // slowest SMs: scripts/sm_fairness.cu).  The next ticket is fetched while the
+        // current row's loads are issued.
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
+            const bool dyn = a.ctr != nullptr;
             int64_t item = 0;
-            for (int64_t r = c; r < a.rows; r += G) {
+            int64_t r = dyn ? (int64_t)atomicAdd(a.ctr, 1ull) : c;
+            while (true) {
+                const int64_t rn = r < a.rows ? (dyn ? (int64_t)atomicAdd(a.ctr, 1ull) : r + G) : r;
                 for (int64_t sg = 0; sg < nseg; ++sg, ++item) {
                     const int b = (int)(item % NBUF);
                     stall_site<STALL>(a.stall, r, sg, 1);
                     if (item >= NBUF) mbar_wait(&freeb[b], (uint32_t)(((item / NBUF) - 1) & 1));
+                    if (r >= a.rows) {  // end marker: the scanners stop at this item
+                        item_row[b] = -1;
+                        mbar_arrive(&full[b]);
+                        break;
+                    }
+                    item_row[b] = r;
+                    item_seg[b] = sg;
                     const int64_t e0 = sg * SEG;
                     const int64_t cnt = (a.cols - e0) < SEG ? (a.cols - e0) : SEG;
                     const uint32_t bytes = (uint32_t)(cnt * sizeof(TIn));
@@ -89,6 +107,17 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
                     char *dst = reinterpret_cast<char *>(buf + (size_t)b * SEG);
                     for (uint32_t o = 0; o < bytes; o += 16384)
                         bulk_g2s(dst + o, src + o, bytes - o < 16384u ? bytes - o : 16384u, &full[b], pol);
+                }
+                if (r >= a.rows) break;
+                r = rn;
+            }
+            if (dyn) {
+                // the last producer to take its final ticket resets the counters for the
+                // next launch on this scratch (stream order makes them visible to it)
+                __threadfence();
+                if (atomicAdd(a.ctr + 1, 1ull) == (unsigned long long)(G - 1)) {
+                    a.ctr[0] = 0;
+                    a.ctr[1] = 0;
                 }
             }
         }
@@ -99,13 +128,16 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
     const uint64_t pol = policy_evict_first();
     const A *seeds = reinterpret_cast<const A *>(a.row_seeds);
     A *totals = reinterpret_cast<A *>(a.row_totals);
-    int64_t item = 0;
-    for (int64_t r = c; r < a.rows; r += G) {
-        A carry = seeds ? seeds[r] : (A)0;
-        for (int64_t sg = 0; sg < nseg; ++sg, ++item) {
+    A carry = (A)0;
+    for (int64_t item = 0;; ++item) {
+        {
             const int b = (int)(item % NBUF);
-            stall_site<STALL>(a.stall, r * 4096 + sg, warp, 2);
             mbar_wait(&full[b], (uint32_t)((item / NBUF) & 1));
+            const int64_t r = item_row[b];
+            if (r < 0) break;
+            const int64_t sg = item_seg[b];
+            stall_site<STALL>(a.stall, r * 4096 + sg, warp, 2);
+            if (sg == 0) carry = seeds ? seeds[r] : (A)0;
             const TIn *sb = buf + (size_t)b * SEG;
             A *tb = tot + b * NCH;
             const int64_t e0 = sg * SEG;
@@ -221,8 +253,8 @@ __global__ void __launch_bounds__((SW + 1) * 32, RPC <= 2 ? 2 : 1) scan_rows_ker
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&freeb[b]);
+            if (sg == nseg - 1 && totals && warp == 0 && lane == 0) totals[r] = carry;
         }
-        if (totals && warp == 0 && lane == 0) totals[r] = carry;
     }
 }
 

@@ -370,6 +370,34 @@ def test_batched_rows_edge_cases(ps, rows_kernel):
         lib.ps_set_tuning(b"rows_kernel", saved)
 
 
+@pytest.mark.parametrize("dynamic", [0, 1])
+def test_rows_kernel_row_tickets(ps, dynamic):
+    """Rows kernel with rows from the grid-wide ticket (1) or fixed shares (0): the
+    same results, and the ticket counters return to zero after every launch (a
+    second and third launch on the same scratch still cover every row once)."""
+    from paper_2312_14874_b200 import _lib, device
+    lib = _lib.load()
+    saved = (lib.ps_get_tuning(b"rows_kernel"), lib.ps_get_tuning(b"rows_dynamic"))
+    lib.ps_set_tuning(b"rows_kernel", 2)
+    lib.ps_set_tuning(b"rows_dynamic", dynamic)
+    try:
+        _batched_cases(device)
+        r = np.random.default_rng(12)
+        for rows, cols in ((5000, 4096), (1200, 40_000)):
+            x = r.integers(0, 256, (rows, cols), dtype=np.int32)
+            exp = np.cumsum(x.astype(np.int64), axis=1)
+            xt = _cuda(x)
+            for _ in range(3):
+                out = torch.full((rows, cols), -1, dtype=torch.int64, device="cuda")
+                tots = torch.full((rows,), -1, dtype=torch.int64, device="cuda")
+                device.scan_batched(xt, out, row_totals=tots)
+                assert np.array_equal(_host(out), exp), (rows, cols, dynamic)
+                assert np.array_equal(_host(tots), exp[:, -1])
+    finally:
+        lib.ps_set_tuning(b"rows_kernel", saved[0])
+        lib.ps_set_tuning(b"rows_dynamic", saved[1])
+
+
 def _batched_cases(device):
     r = np.random.default_rng(8)
     for rows, cols, ld in ((1, 1, 1), (3, 5, 8), (7, 8192, 8192), (5, 8193, 8200), (64, 100_000, 100_000),
