@@ -259,6 +259,8 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "rows_dynamic"     rows kernel: 1 = rows handed out from a grid-wide ticket kept in
  *                      the scratch's control words (faster SMs take more rows),
  *                      0 = CTA c takes rows c, c+G, ... (default 1)
+ *   "rows_multi"       rows kernel: 1 = rows of at most half a 64 KiB buffer share
+ *                      buffers (several rows per TMA item), 0 = one row per buffer
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability

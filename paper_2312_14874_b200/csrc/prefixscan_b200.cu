@@ -85,6 +85,7 @@ struct Tuning {
     int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
     int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
     int rows_dynamic = 1;                   // rows kernel: rows from a grid-wide ticket (0 = fixed shares)
+    int rows_multi = 1;                     // rows kernel: several short rows per buffer (0 = one row per buffer)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
 };
 Tuning g_tune;
@@ -293,6 +294,9 @@ template <> struct RowsCfg<float> { static constexpr int SW = 8, RPC = 2, NBUF =
 #define WKERN scan_rows_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH>
 #define WKERN_STALL \
     scan_rows_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH, true>
+#define WMKERN scan_rows_multi_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH>
+#define WMKERN_STALL \
+    scan_rows_multi_kernel<TIn, TOut, RowsCfg<TIn>::SW, RowsCfg<TIn>::RPC, RowsCfg<TIn>::NBUF, RowsCfg<TIn>::NCH, true>
 
 template <typename TIn, typename TOut>
 int rows_grid() {
@@ -338,9 +342,27 @@ int launch_rows(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     a.vec_out = (uintptr_t)out % 32 == 0 && (ld_out * (int64_t)sizeof(TOut)) % 32 == 0;
     int64_t G = rows_grid<TIn, TOut>();
     if (G > rows) G = rows;
+    // rows of at most half a buffer: several rows per buffer (scan_rows_multi_kernel)
+    const bool multi = cols <= WGEO::SEG / 2 && g_tune.rows_multi;
+    if (multi) {
+        static bool attr[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !attr[dev]) {
+            cudaFuncSetAttribute(WMKERN, cudaFuncAttributeMaxDynamicSharedMemorySize, WGEO::SMEM);
+            attr[dev] = true;
+        }
+    }
     if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
-        cudaFuncSetAttribute(WKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, WGEO::SMEM);
-        WKERN_STALL<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+        if (multi) {
+            cudaFuncSetAttribute(WMKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, WGEO::SMEM);
+            WMKERN_STALL<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+        } else {
+            cudaFuncSetAttribute(WKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, WGEO::SMEM);
+            WKERN_STALL<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
+        }
+    } else if (multi) {
+        WMKERN<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
     } else {
         WKERN<<<(unsigned)G, WGEO::THREADS, WGEO::SMEM, s>>>(a);
     }
@@ -631,6 +653,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "stream_inflight")) {
         if (value < 0 || value > 8) return PS_ERR_ARG;
         g_tune.stream_inflight = (int)value;
+    } else if (!std::strcmp(key, "rows_multi")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.rows_multi = (int)value;
     } else if (!std::strcmp(key, "rows_dynamic")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.rows_dynamic = (int)value;
@@ -673,6 +698,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "select_kernel")) return g_select_kernel;
     if (!std::strcmp(key, "stream_inflight")) return g_tune.stream_inflight;
     if (!std::strcmp(key, "rows_dynamic")) return g_tune.rows_dynamic;
+    if (!std::strcmp(key, "rows_multi")) return g_tune.rows_multi;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;

@@ -398,6 +398,42 @@ def test_rows_kernel_row_tickets(ps, dynamic):
         lib.ps_set_tuning(b"rows_dynamic", saved[1])
 
 
+@pytest.mark.parametrize("multi", [0, 1])
+def test_rows_kernel_short_rows(ps, multi):
+    """Rows of at most half a buffer: several rows per buffer (multi=1, segmented
+    chunk scan per row) or one row per buffer (multi=0); seeds, totals, exclusive,
+    partial last items, every value dtype."""
+    from paper_2312_14874_b200 import _lib, device
+    lib = _lib.load()
+    saved = (lib.ps_get_tuning(b"rows_kernel"), lib.ps_get_tuning(b"rows_multi"))
+    lib.ps_set_tuning(b"rows_kernel", 2)
+    lib.ps_set_tuning(b"rows_multi", multi)
+    try:
+        r = np.random.default_rng(13)
+        for rows, cols in ((5000, 3000), (3001, 12), (2000, 8192), (1999, 4100), (301, 1028), (7, 4)):
+            x = r.integers(0, 256, (rows, cols), dtype=np.int32)
+            seeds = torch.arange(rows, dtype=torch.int64, device="cuda") * 7
+            inc = np.cumsum(x.astype(np.int64), axis=1) + (np.arange(rows) * 7)[:, None]
+            for excl in (False, True):
+                out = torch.full((rows, cols), -1, dtype=torch.int64, device="cuda")
+                tots = torch.full((rows,), -1, dtype=torch.int64, device="cuda")
+                device.scan_batched(_cuda(x), out, exclusive=excl, row_seeds=seeds, row_totals=tots)
+                exp = inc if not excl else np.concatenate([(np.arange(rows) * 7)[:, None], inc[:, :-1]], axis=1)
+                assert np.array_equal(_host(out), exp), (rows, cols, excl, multi)
+                assert np.array_equal(_host(tots), inc[:, -1]), (rows, cols, multi)
+        for dt in (np.float32, np.int64, np.uint32, np.float64):
+            for rows, cols in ((3000, 1000), (500, 2052)):
+                x = GENS[dt](r, rows * cols).reshape(rows, cols)
+                out = torch.empty_like(_cuda(x))
+                tots = torch.empty(rows, dtype=device.acc_dtype(x.dtype), device="cuda")
+                device.scan_batched(_cuda(x), out, row_totals=tots)
+                for i in (0, 1, rows // 2, rows - 1):
+                    _assert_array(_host(out[i]), _expected(x[i]), f"{dt.__name__} row {i} {rows}x{cols}")
+    finally:
+        lib.ps_set_tuning(b"rows_kernel", saved[0])
+        lib.ps_set_tuning(b"rows_multi", saved[1])
+
+
 def _batched_cases(device):
     r = np.random.default_rng(8)
     for rows, cols, ld in ((1, 1, 1), (3, 5, 8), (7, 8192, 8192), (5, 8193, 8200), (64, 100_000, 100_000),
