@@ -263,22 +263,67 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
             if (a.mail.n) carry += mailbox_sum<A>(a.mail, lane);
         }
-        // integer data: next gather issued early and the chunk scan inside the round trip
-        // (int64 2^27 -2 %, cfg1 unchanged); float32: gathers issued on their own turn
-        // (the early poll made cfg2 2.6 % slower: its reducers, not the ledger, set the pace)
-        constexpr bool OVERLAP = !FLOAT;
-        ulonglong2 dn[GATHER_LP];  // the gather in flight (launcher: G <= 32 * GATHER_LP)
-        if (OVERLAP) desc_issue(dn, a.desc, G, lane);
-        for (int64_t r = 0; r < a.rounds; ++r) {
-            const int b = (int)(r % NBUF);
-            stall_site<STALL>(a.stall, r * G + c, 0, 4);
-            const A *tot = chunk_tot + b * MAXC;
-            A *pr = chunk_pre + b * MAXC;
-            A ex = (A)0, t0 = (A)0;
-            auto chunk_prefix = [&]() {  // exclusive scan of this portion's chunk totals
+        if constexpr (FLOAT) {
+            // float32/float64: one gather per region on its own turn, then the fold (the
+            // early-issued gather below made cfg2 2.6 % slower: its reducers, not the
+            // ledger, set the pace)
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                A sb, sa;
+                stall_site<STALL>(a.stall, r * G + c, 0, 4);
+#ifdef PS_EXP_NOLEDGER
+                sb = sa = (A)0;
+#else
+#ifdef PS_TRACE
+                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 3] = gtimer();
+#endif
+                gather_totals<A>(a.desc + r * G, G, c, want, lane, sb, sa);
+#ifdef PS_TRACE
+                    if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
+#endif
+#endif
+
                 mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
+                const A *tot = chunk_tot + b * MAXC;
+                A *pr = chunk_pre + b * MAXC;
                 // nchunk <= 64: two chunks per lane, exclusive scan across the warp
-                t0 = lane * 2 < nchunk ? tot[lane * 2] : (A)0;
+                const A t0 = lane * 2 < nchunk ? tot[lane * 2] : (A)0;
+                const A t1 = lane * 2 + 1 < nchunk ? tot[lane * 2 + 1] : (A)0;
+                const A own = t0 + t1;
+                A incl = own;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const A y = shfl_up(incl, dd);
+                    if (lane >= dd) incl += y;
+                }
+                A ex = shfl_up(incl, 1);
+                if (lane == 0) ex = (A)0;
+                const A base = carry + sb + ex;
+                if (lane * 2 < nchunk) pr[lane * 2] = base;
+                if (lane * 2 + 1 < nchunk) pr[lane * 2 + 1] = base + t0;
+                carry += sa;
+                stall_site<STALL>(a.stall, r * G + c, 0, 5);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pre[b]);
+#ifdef PS_TRACE
+                    if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
+#endif
+            }
+        } else {
+            // integer data: the next region's gather is issued as soon as this one's
+            // descriptors arrived, and the chunk-total scan runs inside the round trip
+            // (int64 2^27 -2.6 %, cfg1 unchanged)
+            ulonglong2 dn[GATHER_LP];  // the gather in flight (launcher: G <= 32 * GATHER_LP)
+            desc_issue(dn, a.desc, G, lane);
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                stall_site<STALL>(a.stall, r * G + c, 0, 4);
+                // exclusive scan of this portion's chunk totals (needs only this CTA's reducers)
+                mbar_wait(&red[b], par(r));  // own chunk totals (and chunk_pre[b] is free, see above)
+                const A *tot = chunk_tot + b * MAXC;
+                A *pr = chunk_pre + b * MAXC;
+                // nchunk <= 64: two chunks per lane, exclusive scan across the warp
+                const A t0 = lane * 2 < nchunk ? tot[lane * 2] : (A)0;
                 const A t1 = lane * 2 + 1 < nchunk ? tot[lane * 2 + 1] : (A)0;
                 A incl = t0 + t1;
 #pragma unroll
@@ -286,47 +331,44 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                     const A y = shfl_up(incl, dd);
                     if (lane >= dd) incl += y;
                 }
-                ex = shfl_up(incl, 1);
+                A ex = shfl_up(incl, 1);
                 if (lane == 0) ex = (A)0;
-            };
-            if (OVERLAP) chunk_prefix();
-            A sb = (A)0, sa = (A)0;
+                A sb = (A)0, sa = (A)0;
 #ifndef PS_EXP_NOLEDGER
 #ifdef PS_TRACE
-            if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 3] = gtimer();
+                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 3] = gtimer();
 #endif
-            if (!OVERLAP) desc_issue(dn, a.desc + r * G, G, lane);
-            desc_wait(dn, a.desc + r * G, G, want, lane);
+                desc_wait(dn, a.desc + r * G, G, want, lane);
 #pragma unroll
-            for (int i = 0; i < GATHER_LP; ++i) {  // gather_totals' summation order
-                const int j = lane + 32 * i;
-                if (j < G) {
-                    const A v = acc_from_bits<A>(dn[i].y);
-                    sa += v;
-                    if (j < c) sb += v;
+                for (int i = 0; i < GATHER_LP; ++i) {  // gather_totals' summation order
+                    const int j = lane + 32 * i;
+                    if (j < G) {
+                        const A v = acc_from_bits<A>(dn[i].y);
+                        sa += v;
+                        if (j < c) sb += v;
+                    }
                 }
-            }
-            if (OVERLAP && r + 1 < a.rounds) desc_issue(dn, a.desc + (r + 1) * G, G, lane);
+                if (r + 1 < a.rounds) desc_issue(dn, a.desc + (r + 1) * G, G, lane);
 #pragma unroll
-            for (int d = 16; d > 0; d >>= 1) {  // both warp sums in one pass
-                sa += __shfl_xor_sync(FULL, sa, d);
-                sb += __shfl_xor_sync(FULL, sb, d);
+                for (int d = 16; d > 0; d >>= 1) {  // both warp sums in one pass
+                    sa += __shfl_xor_sync(FULL, sa, d);
+                    sb += __shfl_xor_sync(FULL, sb, d);
+                }
+#ifdef PS_TRACE
+                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
+#endif
+#endif
+                const A base = carry + sb + ex;
+                if (lane * 2 < nchunk) pr[lane * 2] = base;
+                if (lane * 2 + 1 < nchunk) pr[lane * 2 + 1] = base + t0;
+                carry += sa;
+                stall_site<STALL>(a.stall, r * G + c, 0, 5);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pre[b]);
+#ifdef PS_TRACE
+                if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
+#endif
             }
-#ifdef PS_TRACE
-            if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 4] = gtimer();
-#endif
-#endif
-            if (!OVERLAP) chunk_prefix();
-            const A base = carry + sb + ex;
-            if (lane * 2 < nchunk) pr[lane * 2] = base;
-            if (lane * 2 + 1 < nchunk) pr[lane * 2 + 1] = base + t0;
-            carry += sa;
-            stall_site<STALL>(a.stall, r * G + c, 0, 5);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pre[b]);
-#ifdef PS_TRACE
-            if (g_trace && lane == 0) g_trace[(r * G + c) * 8 + 5] = gtimer();
-#endif
         }
         if (c == 0 && lane == 0 && a.total) *reinterpret_cast<A *>(a.total) = carry;
         return;
