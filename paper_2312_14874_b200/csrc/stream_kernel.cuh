@@ -207,6 +207,32 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             const TIn *sb = buf + (size_t)b * P;
             const int64_t p0 = p0_of(r);
             const bool w = whole(r);
+            if (FLOAT && w && nchunk == 2 * RWP) {
+                // float data, whole portion, two chunks per reducer warp: both reduced
+                // together (the TwoSum reducer is latency-bound next to 8 scanner warps;
+                // cfg2 +0.7 %; integer data measured 1 % slower this way)
+                const int64_t c0 = rw, c1 = rw + RWP;
+                A s0 = (A)0, s1 = (A)0;
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) {
+                    const V256 r0 = lds256<(sizeof(TIn) == 8)>(sb + c0 * CHUNK + rr * ROW_ELEMS + lane * VEC);
+                    const V256 r1 = lds256<(sizeof(TIn) == 8)>(sb + c1 * CHUNK + rr * ROW_ELEMS + lane * VEC);
+                    TIn x0[VEC], x1[VEC];
+                    unpack<TIn>(r0, x0);
+                    unpack<TIn>(r1, x1);
+                    s0 += lane_row_sum<TIn, A, VEC>(x0);
+                    s1 += lane_row_sum<TIn, A, VEC>(x1);
+                }
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) {
+                    s0 += __shfl_xor_sync(FULL, s0, d);
+                    s1 += __shfl_xor_sync(FULL, s1, d);
+                }
+                if (lane == 0) {
+                    tot[c0] = s0;
+                    tot[c1] = s1;
+                }
+            } else
             for (int64_t ch = rw; ch < nchunk; ch += RWP) {
                 A s = (A)0;
                 if (w) {
