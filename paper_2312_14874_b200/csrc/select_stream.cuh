@@ -189,14 +189,13 @@ __global__ void __launch_bounds__(SS_THREADS, 1) select_stream_kernel(const Sele
     if (warp == W_LEDGER) {
         // ---------------- ledger: per-chunk output offsets -----------------------------
         long long carry = 0;
+        // the next region's gather is issued as soon as this one's descriptors arrived
+        // and the chunk scan runs inside the round trip (as in scan_stream_kernel)
+        const bool overlap = G <= 32 * GATHER_LP;
+        ulonglong2 dn[GATHER_LP];
+        if (overlap) desc_issue(dn, a.desc, G, lane);
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
-            long long sb, sa;
-#ifdef PS_EXP_NOLEDGER
-            sb = sa = 0;
-#else
-            gather_totals<long long>(a.desc + r * G, G, c, a.want, lane, sb, sa);
-#endif
             mbar_wait(&red[b], par(r));
             const long long *tot = chunk_tot + b * SS_SW;
             long long *pr = chunk_pre + b * SS_SW;
@@ -207,6 +206,29 @@ __global__ void __launch_bounds__(SS_THREADS, 1) select_stream_kernel(const Sele
                 const long long y = __shfl_up_sync(FULL, inc, d);
                 if (lane >= d) inc += y;
             }
+            long long sb = 0, sa = 0;
+#ifndef PS_EXP_NOLEDGER
+            if (overlap) {
+                desc_wait(dn, a.desc + r * G, G, a.want, lane);
+#pragma unroll
+                for (int i = 0; i < GATHER_LP; ++i) {  // gather_totals' order
+                    const int j = lane + 32 * i;
+                    if (j < G) {
+                        const long long v = (long long)dn[i].y;
+                        sa += v;
+                        if (j < c) sb += v;
+                    }
+                }
+                if (r + 1 < a.rounds) desc_issue(dn, a.desc + (r + 1) * G, G, lane);
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) {
+                    sa += __shfl_xor_sync(FULL, sa, d);
+                    sb += __shfl_xor_sync(FULL, sb, d);
+                }
+            } else {
+                gather_totals<long long>(a.desc + r * G, G, c, a.want, lane, sb, sa);
+            }
+#endif
             if (lane < SS_SW) pr[lane] = carry + sb + inc - t;
             carry += sa;
             __syncwarp();

@@ -79,6 +79,15 @@ int main() {
         run<float, float, 8, 4, 6, 4>("f32_26", in, out, S * 4, scratch, epoch, 32 << 10);
         return 0;
     }
+    if (getenv("F32GEO")) {  // float32 scanner/reducer geometry
+        run<float, float, 8, 4, 6, 4>("f32 8x4 r4", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 16, 2, 6, 4>("f32 16x2 r4", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 16, 2, 6, 8>("f32 16x2 r8", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 8, 2, 6, 4>("f32 8x2 r4", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 12, 2, 6, 4>("f32 12x2 r4", in, out, N, scratch, epoch, 24 << 10);
+        run<float, float, 8, 4, 6, 4>("f32 8x4 r4", in, out, N, scratch, epoch, 32 << 10);
+        return 0;
+    }
     run<float, float, 8, 4, 6, 4>("f32_28", in, out, N, scratch, epoch, 32 << 10);
     run<int64_t, int64_t, 8, 4, 6, 4>("i64_24", in, out, S, scratch, epoch, 32 << 10);
     run<int64_t, int64_t, 8, 4, 6, 4>("i64_27", in, out, N / 2, scratch, epoch, 32 << 10);
