@@ -22,6 +22,7 @@ struct SegArgs {
     const int64_t *offsets;  // nseg + 1 entries
     int64_t nseg;
     void *totals;  // acc-typed per segment (pre-zeroed by the host)
+    const int64_t *tile_seg;  // [tiles]: segment holding each tile's first element (seg_tile_kernel)
     Desc desc;
     uint32_t epoch;
     int exclusive;
@@ -38,6 +39,49 @@ __device__ __forceinline__ int64_t seg_of(const int64_t *off, int64_t nseg, int6
     }
     return lo;
 }
+
+// Segment of every tile's first element, one thread per tile: a galloping search
+// from the guess e * nseg / n (uniform segments: a couple of dependent loads), so
+// the scan kernel needs no per-lane binary searches over the whole offsets array
+// (each was ~log2(nseg) dependent L2 round trips under full load).
+__global__ void seg_tile_kernel(const int64_t *off, int64_t nseg, int64_t n, int64_t lead, int64_t tile_elems,
+                                int64_t tiles, int64_t *tile_seg) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= tiles) return;
+    int64_t e = t * tile_elems - lead;
+    if (e < 0) e = 0;
+    if (e > n - 1) e = n - 1;
+    // largest s in [0, nseg) with off[s] <= e (off[0] == 0 <= e)
+    int64_t g = (int64_t)((double)e / (double)n * (double)nseg);
+    if (g > nseg - 1) g = nseg - 1;
+    if (g < 0) g = 0;
+    int64_t lo, hi;  // invariant: off[lo] <= e, answer < hi
+    if (__ldg(off + g) <= e) {
+        lo = g;
+        int64_t step = 1;
+        while (lo + step < nseg && __ldg(off + lo + step) <= e) {
+            lo += step;
+            step <<= 1;
+        }
+        hi = lo + step < nseg ? lo + step : nseg;
+    } else {
+        hi = g;
+        int64_t step = 1;
+        while (hi - step > 0 && __ldg(off + hi - step) > e) {
+            hi -= step;
+            step <<= 1;
+        }
+        lo = hi - step > 0 ? hi - step : 0;
+    }
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= e) lo = mid;
+        else hi = mid;
+    }
+    tile_seg[t] = lo;
+}
+
+constexpr int SEG_CACHE = 4096;  // offsets of one tile's segments kept in shared memory (2 CTAs/SM by registers anyway)
 
 template <typename A> struct Pair {
     A v;
@@ -59,6 +103,7 @@ __global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
     __shared__ A s_wv[WARPS];
     __shared__ int s_wf[WARPS];
     __shared__ A s_base[WARPS];
+    __shared__ int64_t s_off[SEG_CACHE];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t tile = blockIdx.x;
@@ -86,6 +131,25 @@ __global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
             }
     }
 
+    // this tile's segments are [s_lo, s_hi]; their offsets (s_lo .. s_hi + 1) are
+    // cached in shared memory when they fit, so every lookup below is local
+    const int64_t s_lo = a.tile_seg[tile];
+    const int64_t s_hi = tile + 1 < (int64_t)gridDim.x ? a.tile_seg[tile + 1] : a.nseg - 1;
+    const bool cached = s_hi - s_lo + 2 <= SEG_CACHE;
+    if (cached)
+        for (int64_t i = threadIdx.x; i <= s_hi - s_lo + 1; i += blockDim.x) s_off[i] = __ldg(a.offsets + s_lo + i);
+    __syncthreads();
+    auto off_at = [&](int64_t sg) { return cached ? s_off[sg - s_lo] : __ldg(a.offsets + sg); };
+    auto seg_at = [&](int64_t e) {  // largest s in [s_lo, s_hi] with off[s] <= e
+        int64_t lo = s_lo, hi = s_hi + 1;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (off_at(mid) <= e) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+
     // segment heads inside this thread's elements (bit r*VEC + j); element e
     // is a head iff it starts a non-empty segment: off[seg_of(e)] == e
     uint32_t heads = 0;
@@ -99,13 +163,13 @@ __global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
             const int64_t e = e0 + j;
             if (e < 0 || e >= a.n) continue;
             if (s < 0) {
-                s = seg_of(a.offsets, a.nseg, e);
-                nb = __ldg(a.offsets + s + 1);
-                if (__ldg(a.offsets + s) == e) heads |= 1u << (r * VEC + j);
+                s = seg_at(e);
+                nb = off_at(s + 1);
+                if (off_at(s) == e) heads |= 1u << (r * VEC + j);
                 seg0[r] = s;
             } else if (e == nb) {
-                while (__ldg(a.offsets + s + 1) <= e) ++s;
-                nb = __ldg(a.offsets + s + 1);
+                while (off_at(s + 1) <= e) ++s;
+                nb = off_at(s + 1);
                 heads |= 1u << (r * VEC + j);
             }
         }
@@ -188,9 +252,9 @@ __global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
             const int64_t e = t0 + my0 + r * ROW_ELEMS + j - a.lead;
             if (tot && e >= 0 && e < a.n) {
                 if (h) {
-                    while (__ldg(a.offsets + s + 1) <= e) ++s;
+                    while (off_at(s + 1) <= e) ++s;
                 }
-                if (e + 1 == __ldg(a.offsets + s + 1)) tot[s] = run;
+                if (e + 1 == off_at(s + 1)) tot[s] = run;
             }
         }
         if (full) {
@@ -214,7 +278,7 @@ inline int64_t seg_tile_elems(int elem_bytes) { return (int64_t)8 * 4 * 32 * (32
 
 inline size_t seg_scratch_bytes(int64_t n, int elem_bytes) {
     const int64_t tiles = (n + seg_tile_elems(elem_bytes) - 1) / seg_tile_elems(elem_bytes) + 1;
-    return 256 + seg_align_up((size_t)tiles * 16, 256);
+    return 256 + seg_align_up((size_t)tiles * 16, 256) + seg_align_up((size_t)tiles * 8, 256);
 }
 
 template <typename TIn, typename TOut>
@@ -239,6 +303,11 @@ int launch_segmented(const void *in, void *out, int64_t n, const int64_t *offset
     const int64_t tiles = (a.lead + n + TILE - 1) / TILE;
     if (tiles > 0x7fffffffLL) return 2;
     a.desc.d = reinterpret_cast<ulonglong2 *>(static_cast<char *>(scratch) + 256);
+    // tile -> first segment, after the descriptors (seg_scratch_bytes reserves tiles + 1 of each)
+    const int64_t cap = (n + TILE - 1) / TILE + 1;
+    int64_t *tile_seg = reinterpret_cast<int64_t *>(static_cast<char *>(scratch) + 256 + seg_align_up((size_t)cap * 16, 256));
+    a.tile_seg = tile_seg;
+    seg_tile_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(offsets, nseg, n, a.lead, TILE, tiles, tile_seg);
     seg_scan_kernel<TIn, TOut, 8, 4><<<(unsigned)tiles, 256, 0, s>>>(a);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : 1000 + (int)e;

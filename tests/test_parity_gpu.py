@@ -460,6 +460,52 @@ def _batched_cases(device):
                 _assert_array(_host(out[i]), _expected(x[i]), f"{dt.__name__} row {i} {rows}x{cols}")
 
 
+def test_segmented_distributions(ps):
+    """CSR segmented scan over segment-length distributions that exercise the tile ->
+    segment pre-pass (galloping search from the uniform guess) and both offset paths
+    (cached in shared memory, and tiles with more than SEG_CACHE segments): long
+    uniform, geometric (skewed), runs of empty segments, length-1 segments, an
+    unaligned view; totals and exclusive; int32 -> int64 and float32."""
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(21)
+    n = 3_000_003
+    cases = {
+        "uniform": np.sort(r.integers(0, n + 1, 300)),
+        "geometric": np.cumsum(r.geometric(1 / 40, 200_000)),
+        "empties": np.sort(np.concatenate([r.integers(0, n + 1, 5000), np.repeat(r.integers(0, n + 1, 50), 200)])),
+        "ones": np.arange(1, n),
+        "few": np.array([n // 2]),
+    }
+    for name, cuts in cases.items():
+        cuts = cuts[(cuts > 0) & (cuts < n)]
+        offs = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+        nseg = len(offs) - 1
+        x = r.integers(0, 1000, n + 1, dtype=np.int32)
+        for view in (False, True):
+            xs = x[1:] if view else x[:n]
+            xt = _cuda(x)[1:] if view else _cuda(x)[:n]
+            for excl in (False, True):
+                out = torch.empty(n, dtype=torch.int64, device="cuda")
+                tots = torch.empty(nseg, dtype=torch.int64, device="cuda")
+                device.scan_segmented(xt, _cuda(offs), out, exclusive=excl, seg_totals=tots)
+                c = np.cumsum(xs.astype(np.int64))
+                starts = np.repeat(offs[:-1], np.diff(offs))
+                before = np.where(starts > 0, c[np.maximum(starts - 1, 0)], 0)
+                inc = c - before
+                exp = inc - xs if excl else inc
+                assert np.array_equal(_host(out), exp), (name, view, excl)
+                ends = offs[1:] - 1
+                exp_tot = np.where(np.diff(offs) > 0, c[np.maximum(ends, 0)] - np.where(offs[:-1] > 0, c[np.maximum(offs[:-1] - 1, 0)], 0), 0)
+                assert np.array_equal(_host(tots), exp_tot), (name, view)
+        f = r.random(n, dtype=np.float32)
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        device.scan_segmented(_cuda(f), _cuda(offs), out)
+        c = np.cumsum(f.astype(np.float64))
+        starts = np.repeat(offs[:-1], np.diff(offs))
+        before = np.where(starts > 0, c[np.maximum(starts - 1, 0)], 0.0)
+        np.testing.assert_allclose(_host(out), (c - before).astype(np.float32), rtol=1e-5, atol=1e-4, err_msg=name)
+
+
 def test_segmented(ps):
     from paper_2312_14874_b200 import device
     r = np.random.default_rng(9)
