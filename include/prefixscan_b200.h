@@ -261,6 +261,10 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *                      0 = CTA c takes rows c, c+G, ... (default 1)
  *   "rows_multi"       rows kernel: 1 = rows of at most half a 64 KiB buffer share
  *                      buffers (several rows per TMA item), 0 = one row per buffer
+ *   "tiles_row_lead"   batched rows on the look-back tiles kernel (row lengths not a
+ *                      multiple of 16 bytes): 1 = each row's tile grid starts on its own
+ *                      32-byte boundary (vector accesses) and short contiguous rows
+ *                      without seeds run as one uniform-segment scan; 0 = shared lead
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability

@@ -86,6 +86,7 @@ struct Tuning {
     int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
     int rows_dynamic = 1;                   // rows kernel: rows from a grid-wide ticket (0 = fixed shares)
     int rows_multi = 1;                     // rows kernel: several short rows per buffer (0 = one row per buffer)
+    int tiles_row_lead = 1;                 // look-back tiles, batched: 32-byte tile grid per row (0 = shared lead)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
 };
 Tuning g_tune;
@@ -401,6 +402,14 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     if (vec && lead * (int64_t)sizeof(TOut) >= 32) vec = false;
     a.vec_ok = vec;
     a.lead = vec ? lead : 0;
+    // batched rows on element-aligned buffers: lead and vector accesses decided per row
+    // in the kernel (tiles_per_row then has room for the largest lead)
+    int64_t max_lead = 0;
+    if (rows > 1 && g_tune.tiles_row_lead && (uintptr_t)in % sizeof(TIn) == 0 && (uintptr_t)out % sizeof(TOut) == 0) {
+        a.row_lead = 1;
+        a.lead = 0;
+        max_lead = 32 / (int64_t)sizeof(TIn) - 1;
+    }
     const bool big = cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes;
     if (rows == 1 && vec &&
         (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big && stream_grid<TIn, TOut>() <= STREAM_MAX_GRID)))
@@ -409,7 +418,13 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     if (rows == 1 && vec && g_tune.scan_kernel == 2)
         return launch_rounds<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
                                         scratch, scratch_bytes, epoch, s, mail);
-    a.tiles_per_row = (a.lead + cols + TILE - 1) / TILE;
+    // many short contiguous rows without seeds: one flat segmented scan with uniform
+    // segments (a look-back tile per row would leave most of each tile idle)
+    if (rows > 1 && g_tune.tiles_row_lead && !seed_terms && seed_bits == 0 && !mail && ld_in == cols && ld_out == cols &&
+        cols * 4 <= TILE && scratch && scratch_bytes >= seg_scratch_bytes(rows * cols, (int)sizeof(TIn)))
+        return launch_segmented<TIn, TOut>(in, out, rows * cols, nullptr, rows, exclusive, totals, scratch, epoch, s,
+                                           cols);
+    a.tiles_per_row = (a.lead + max_lead + cols + TILE - 1) / TILE;
     const int64_t tiles = rows * a.tiles_per_row;
     if (tiles > 0x7fffffffLL) return PS_ERR_ARG;
     if (a.tiles_per_row > 1) {
@@ -653,6 +668,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "stream_inflight")) {
         if (value < 0 || value > 8) return PS_ERR_ARG;
         g_tune.stream_inflight = (int)value;
+    } else if (!std::strcmp(key, "tiles_row_lead")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.tiles_row_lead = (int)value;
     } else if (!std::strcmp(key, "rows_multi")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.rows_multi = (int)value;
@@ -699,6 +717,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "stream_inflight")) return g_tune.stream_inflight;
     if (!std::strcmp(key, "rows_dynamic")) return g_tune.rows_dynamic;
     if (!std::strcmp(key, "rows_multi")) return g_tune.rows_multi;
+    if (!std::strcmp(key, "tiles_row_lead")) return g_tune.tiles_row_lead;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;

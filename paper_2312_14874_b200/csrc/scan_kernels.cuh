@@ -61,6 +61,7 @@ struct ScanArgs {
     uint32_t epoch;
     int exclusive;
     int vec_ok;             // in/out row bases (minus lead) are 32B aligned
+    int row_lead;           // rows > 1: lead and vec_ok per row from the row's own addresses
     int debug_flags;        // bit 0: skip the look-back (timing experiments only; wrong results)
     Stall stall;            // stress tests: stall injection at the publication points
     Mailbox mail;           // rows == 1: seed += totals published by the ranks before this one
@@ -120,11 +121,28 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int64_t head = row * a.tiles_per_row;
 
     // tile-space coordinates: element c of the row sits at position c + lead
+    int64_t lead = a.lead;
+    bool vec = a.vec_ok;
+    if (a.row_lead) {
+        // each row's tiles start on the 32-byte boundary at or before the row start, so
+        // rows whose length is not a multiple of 32 bytes still move with 256-bit
+        // accesses; contiguous int32 -> int64 and same-size rows then also have their
+        // output 32-byte aligned (checked per row)
+        const uintptr_t ia = (uintptr_t)(reinterpret_cast<const TIn *>(a.in) + row * a.ld_in);
+        lead = (int64_t)((ia & 31) / sizeof(TIn));
+        const uintptr_t oa = (uintptr_t)(reinterpret_cast<TOut *>(a.out) + row * a.ld_out) - lead * sizeof(TOut);
+        vec = (oa & 31) == 0;
+    }
     const int64_t t0 = chunk * TILE;
-    const int64_t lo = a.lead, hi = a.lead + a.cols;  // valid positions [lo, hi)
-    const TIn *in = reinterpret_cast<const TIn *>(a.in) + row * a.ld_in - a.lead + t0;
-    TOut *out = reinterpret_cast<TOut *>(a.out) + row * a.ld_out - a.lead + t0;
-    const bool full = a.vec_ok && t0 >= lo && t0 + TILE <= hi;
+    const int64_t lo = lead, hi = lead + a.cols;  // valid positions [lo, hi)
+    const TIn *in = reinterpret_cast<const TIn *>(a.in) + row * a.ld_in - lead + t0;
+    TOut *out = reinterpret_cast<TOut *>(a.out) + row * a.ld_out - lead + t0;
+    const bool full = vec && t0 >= lo && t0 + TILE <= hi;
+    // a lane's 32-byte vector of row r lies entirely inside the valid positions
+    auto lane_vec = [&](int r) {
+        const int64_t p = t0 + (int64_t)warp * WARP_ELEMS + lane * VEC + r * ROW_ELEMS;
+        return vec && p >= lo && p + VEC <= hi;
+    };
 #ifdef PS_TRACE
     if (g_trace && threadIdx.x == 0) {
         g_trace[tile * 8 + 0] = gtimer();
@@ -143,14 +161,19 @@ __global__ void __launch_bounds__(WARPS * 32)
         for (int r = 0; r < ROWS; ++r) raw[r] = ldg256_stream(in + my0 + r * ROW_ELEMS);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) unpack<TIn>(raw[r], x[r]);
-    } else {
+    } else {  // edge tile: whole lane vectors where they are valid, masked elements elsewhere
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r)
+        for (int r = 0; r < ROWS; ++r) {
+            if (lane_vec(r)) {
+                unpack<TIn>(ldg256_stream(in + my0 + r * ROW_ELEMS), x[r]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) {
-                const int64_t pos = t0 + my0 + r * ROW_ELEMS + j;
-                x[r][j] = (pos >= lo && pos < hi) ? in[my0 + r * ROW_ELEMS + j] : (TIn)0;
+                for (int j = 0; j < VEC; ++j) {
+                    const int64_t pos = t0 + my0 + r * ROW_ELEMS + j;
+                    x[r][j] = (pos >= lo && pos < hi) ? in[my0 + r * ROW_ELEMS + j] : (TIn)0;
+                }
             }
+        }
     }
 
     // ---- per-lane sums, then ROWS interleaved warp scans (5 shuffle rounds) --------
@@ -273,12 +296,25 @@ __global__ void __launch_bounds__(WARPS * 32)
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
             A run = wbase + lex[r];
+            TOut y[VEC];
 #pragma unroll
             for (int j = 0; j < VEC; ++j) {
-                const int64_t pos = t0 + my0 + r * ROW_ELEMS + j;
                 const A before = run;
                 run += (A)x[r][j];
-                if (pos >= lo && pos < hi) out[my0 + r * ROW_ELEMS + j] = (TOut)(a.exclusive ? before : run);
+                y[j] = (TOut)(a.exclusive ? before : run);
+            }
+            if (lane_vec(r)) {
+                constexpr int NV = VEC * sizeof(TOut) / 32;
+#pragma unroll
+                for (int k = 0; k < NV; ++k)
+                    stg256_stream(out + my0 + r * ROW_ELEMS + k * (32 / sizeof(TOut)),
+                                  pack<TOut>(&y[k * (32 / sizeof(TOut))]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    const int64_t pos = t0 + my0 + r * ROW_ELEMS + j;
+                    if (pos >= lo && pos < hi) out[my0 + r * ROW_ELEMS + j] = y[j];
+                }
             }
         }
     }

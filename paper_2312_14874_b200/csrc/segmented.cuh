@@ -23,6 +23,7 @@ struct SegArgs {
     int64_t nseg;
     void *totals;  // acc-typed per segment (pre-zeroed by the host)
     const int64_t *tile_seg;  // [tiles]: segment holding each tile's first element (seg_tile_kernel)
+    int64_t ucols;            // > 0: uniform segments of ucols elements (contiguous batched rows), no offsets
     Desc desc;
     uint32_t epoch;
     int exclusive;
@@ -133,13 +134,24 @@ __global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
 
     // this tile's segments are [s_lo, s_hi]; their offsets (s_lo .. s_hi + 1) are
     // cached in shared memory when they fit, so every lookup below is local
-    const int64_t s_lo = a.tile_seg[tile];
-    const int64_t s_hi = tile + 1 < (int64_t)gridDim.x ? a.tile_seg[tile + 1] : a.nseg - 1;
-    const bool cached = s_hi - s_lo + 2 <= SEG_CACHE;
+    int64_t s_lo, s_hi;
+    if (a.ucols) {  // uniform segments: everything is arithmetic
+        const int64_t e_first = t0 - a.lead > 0 ? t0 - a.lead : 0;
+        const int64_t e_next = t0 + TILE - a.lead < a.n ? t0 + TILE - a.lead : a.n - 1;
+        s_lo = e_first / a.ucols;
+        s_hi = e_next / a.ucols;
+    } else {
+        s_lo = a.tile_seg[tile];
+        s_hi = tile + 1 < (int64_t)gridDim.x ? a.tile_seg[tile + 1] : a.nseg - 1;
+    }
+    const bool cached = !a.ucols && s_hi - s_lo + 2 <= SEG_CACHE;
     if (cached)
         for (int64_t i = threadIdx.x; i <= s_hi - s_lo + 1; i += blockDim.x) s_off[i] = __ldg(a.offsets + s_lo + i);
     __syncthreads();
-    auto off_at = [&](int64_t sg) { return cached ? s_off[sg - s_lo] : __ldg(a.offsets + sg); };
+    auto off_at = [&](int64_t sg) {
+        if (a.ucols) return sg * a.ucols < a.n ? sg * a.ucols : a.n;
+        return cached ? s_off[sg - s_lo] : __ldg(a.offsets + sg);
+    };
     auto seg_at = [&](int64_t e) {  // largest s in [s_lo, s_hi] with off[s] <= e
         int64_t lo = s_lo, hi = s_hi + 1;
         while (hi - lo > 1) {
@@ -283,7 +295,7 @@ inline size_t seg_scratch_bytes(int64_t n, int elem_bytes) {
 
 template <typename TIn, typename TOut>
 int launch_segmented(const void *in, void *out, int64_t n, const int64_t *offsets, int64_t nseg, int exclusive,
-                     void *totals, void *scratch, uint32_t epoch, cudaStream_t s) {
+                     void *totals, void *scratch, uint32_t epoch, cudaStream_t s, int64_t ucols = 0) {
     constexpr int64_t TILE = (int64_t)8 * 4 * 32 * (32 / sizeof(TIn));
     SegArgs a{};
     a.in = in;
@@ -307,7 +319,9 @@ int launch_segmented(const void *in, void *out, int64_t n, const int64_t *offset
     const int64_t cap = (n + TILE - 1) / TILE + 1;
     int64_t *tile_seg = reinterpret_cast<int64_t *>(static_cast<char *>(scratch) + 256 + seg_align_up((size_t)cap * 16, 256));
     a.tile_seg = tile_seg;
-    seg_tile_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(offsets, nseg, n, a.lead, TILE, tiles, tile_seg);
+    a.ucols = ucols;
+    if (!ucols)
+        seg_tile_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(offsets, nseg, n, a.lead, TILE, tiles, tile_seg);
     seg_scan_kernel<TIn, TOut, 8, 4><<<(unsigned)tiles, 256, 0, s>>>(a);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : 1000 + (int)e;

@@ -434,6 +434,53 @@ def test_rows_kernel_short_rows(ps, multi):
         lib.ps_set_tuning(b"rows_multi", saved[1])
 
 
+@pytest.mark.parametrize("row_lead", [0, 1])
+def test_tiles_rows_unaligned_lengths(ps, row_lead):
+    """Batched rows whose length is not a multiple of 16 bytes take the look-back
+    tiles kernel; with row_lead each row's tile grid starts on its own 32-byte
+    boundary (vector accesses inside, masked edges).  Strided and offset views,
+    every dtype pair family, seeds, totals, exclusive."""
+    from paper_2312_14874_b200 import _lib, device
+    lib = _lib.load()
+    saved = lib.ps_get_tuning(b"tiles_row_lead")
+    lib.ps_set_tuning(b"tiles_row_lead", row_lead)
+    try:
+        r = np.random.default_rng(14)
+        for rows, cols, ld, off in ((300, 16383, 16383, 0), (257, 16385, 16390, 3), (1000, 250, 250, 0),
+                                    (64, 70_001, 70_001, 1), (999, 13, 13, 5), (40, 8191, 8200, 2),
+                                    (5000, 1, 1, 0), (3000, 2047, 2047, 1), (700, 2049, 2049, 0)):
+            x = r.integers(0, 256, (rows * ld + off,), dtype=np.int32)
+            xv = x[off:].reshape(rows, ld)[:, :cols]
+            xt = _cuda(x)[off:].reshape(rows, ld)[:, :cols]
+            seeds = torch.arange(rows, dtype=torch.int64, device="cuda") * 3
+            inc = np.cumsum(xv.astype(np.int64), axis=1) + (np.arange(rows) * 3)[:, None]
+            for excl in (False, True):
+                out = torch.full((rows, cols), -1, dtype=torch.int64, device="cuda")
+                tots = torch.full((rows,), -1, dtype=torch.int64, device="cuda")
+                device.scan_batched(xt, out, exclusive=excl, row_seeds=seeds, row_totals=tots)
+                exp = inc if not excl else np.concatenate([(np.arange(rows) * 3)[:, None], inc[:, :-1]], axis=1)
+                assert np.array_equal(_host(out), exp), (rows, cols, ld, off, excl, row_lead)
+                assert np.array_equal(_host(tots), inc[:, -1]), (rows, cols, ld, off, row_lead)
+            # no seeds: short contiguous rows go through the uniform-segment scan
+            plain = np.cumsum(xv.astype(np.int64), axis=1)
+            for excl in (False, True):
+                out = torch.full((rows, cols), -1, dtype=torch.int64, device="cuda")
+                tots = torch.full((rows,), -1, dtype=torch.int64, device="cuda")
+                device.scan_batched(xt, out, exclusive=excl, row_totals=tots)
+                exp = plain if not excl else plain - xv
+                assert np.array_equal(_host(out), exp), ("noseed", rows, cols, ld, off, excl, row_lead)
+                assert np.array_equal(_host(tots), plain[:, -1]), ("noseed", rows, cols, ld, off, row_lead)
+        for dt in (np.float32, np.int64, np.uint32):
+            for rows, cols in ((300, 5001), (50, 33_333), (2000, 777)):
+                x = GENS[dt](r, rows * cols).reshape(rows, cols)
+                out = torch.empty_like(_cuda(x))
+                device.scan_batched(_cuda(x), out)
+                for i in (0, 1, rows // 2, rows - 1):
+                    _assert_array(_host(out[i]), _expected(x[i]), f"{dt.__name__} row {i} {rows}x{cols}")
+    finally:
+        lib.ps_set_tuning(b"tiles_row_lead", saved)
+
+
 def _batched_cases(device):
     r = np.random.default_rng(8)
     for rows, cols, ld in ((1, 1, 1), (3, 5, 8), (7, 8192, 8192), (5, 8193, 8200), (64, 100_000, 100_000),
