@@ -68,6 +68,16 @@ def elem_bits(value, code: int) -> int:
     return int(value) & 0xFFFFFFFFFFFFFFFF
 
 
+_PAIR_OK: dict = {}
+
+
+def _pair_ok(lib, ci: int, co: int) -> bool:
+    ok = _PAIR_OK.get((ci, co))
+    if ok is None:
+        ok = _PAIR_OK[(ci, co)] = bool(lib.ps_pair_supported(ci, co))
+    return ok
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -107,8 +117,11 @@ _scratch: dict[tuple[int, int], _Scratch] = {}
 _scratch_lock = threading.Lock()
 
 
-def _scratch_for(device: torch.device, nbytes: int, n_epochs: int = 1, kind: str = "lookback"):
-    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream_ptr(device), kind)
+def _scratch_for(device: torch.device, nbytes: int, n_epochs: int = 1, kind: str = "lookback",
+                 stream: int | None = None):
+    if stream is None:
+        stream = _stream_ptr(device)
+    key = (device.index if device.index is not None else torch.cuda.current_device(), stream, kind)
     with _scratch_lock:
         s = _scratch.get(key)
         if s is None:
@@ -139,7 +152,7 @@ def scan(x: torch.Tensor, out: torch.Tensor | None = None, *, exclusive: bool = 
         raise ValueError("output buffer must match input shape")
     ci, co = dtype_code(x.dtype), dtype_code(out.dtype)
     lib = _lib.load()
-    if not lib.ps_pair_supported(ci, co):
+    if not _pair_ok(lib, ci, co):
         raise ValueError(f"unsupported dtype pair {x.dtype} -> {out.dtype}")
     if total is None:
         total = torch.empty(1, dtype=_ACC_TORCH[ci], device=x.device)
@@ -150,9 +163,10 @@ def scan(x: torch.Tensor, out: torch.Tensor | None = None, *, exclusive: bool = 
             raise ValueError(f"seed_terms must be contiguous {_ACC_TORCH[ci]}")
         n_terms = seed_terms.numel()
     n = x.numel()
-    sptr, sbytes, epoch = _scratch_for(x.device, lib.ps_scan_scratch_bytes(n, ci, co))
-    rc = lib.ps_scan(_ptr(x), _ptr(out), n, ci, co, int(bool(exclusive)), acc_bits(seed, ci),
-                     _ptr(seed_terms), n_terms, _ptr(total), sptr, sbytes, epoch, _stream_ptr(x.device))
+    stream = _stream_ptr(x.device)  # once per call: the small-input path is host-bound
+    sptr, sbytes, epoch = _scratch_for(x.device, lib.ps_scan_scratch_bytes(n, ci, co), stream=stream)
+    rc = lib.ps_scan(x.data_ptr(), out.data_ptr(), n, ci, co, int(bool(exclusive)), acc_bits(seed, ci),
+                     _ptr(seed_terms), n_terms, total.data_ptr(), sptr, sbytes, epoch, stream)
     _lib.check(rc, "ps_scan")
     return total
 
