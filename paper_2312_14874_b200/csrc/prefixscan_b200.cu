@@ -1211,7 +1211,8 @@ int ps_select(const void *values, const void *flags, int64_t n, int dtype_values
 #undef ONE
     }
     char *base = static_cast<char *>(scratch);
-    long long *total = count_out ? static_cast<long long *>(count_out) : reinterpret_cast<long long *>(base);
+    // (control word 16: words 0-1 are the rows kernel's row ticket when a scratch is shared)
+    long long *total = count_out ? static_cast<long long *>(count_out) : reinterpret_cast<long long *>(base + 16);
     long long *counts = reinterpret_cast<long long *>(base + 256);
     const uintptr_t va = (uintptr_t)values, fa = (uintptr_t)flags;
     const int vec_ok = (va % 32 == 0) && (fb == 1 ? fa % 8 == 0 : fa % 32 == 0);

@@ -79,7 +79,10 @@ __global__ void seg_tile_kernel(const int64_t *off, int64_t nseg, int64_t n, int
         if (__ldg(off + mid) <= e) lo = mid;
         else hi = mid;
     }
-    tile_seg[t] = lo;
+    // stored as lo << 2: the low two bits of every word stay 0, so no word of this
+    // array can ever pass for a published look-back descriptor (status != 0) when a
+    // later scan reuses the scratch with a small epoch
+    tile_seg[t] = lo << 2;
 }
 
 constexpr int SEG_CACHE = 4096;  // offsets of one tile's segments kept in shared memory (2 CTAs/SM by registers anyway)
@@ -141,8 +144,8 @@ __global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
         s_lo = e_first / a.ucols;
         s_hi = e_next / a.ucols;
     } else {
-        s_lo = a.tile_seg[tile];
-        s_hi = tile + 1 < (int64_t)gridDim.x ? a.tile_seg[tile + 1] : a.nseg - 1;
+        s_lo = a.tile_seg[tile] >> 2;
+        s_hi = tile + 1 < (int64_t)gridDim.x ? (a.tile_seg[tile + 1] >> 2) : a.nseg - 1;
     }
     const bool cached = !a.ucols && s_hi - s_lo + 2 <= SEG_CACHE;
     if (cached)

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_count_kernel(const TF *fla
             long long tot = 0;
 #pragma unroll
             for (int w = 0; w < SEL_WARPS; ++w) tot += s_warp[w];
-            counts[t] = tot;
+            counts[t] = tot << 2;  // low 2 bits 0: never a published look-back descriptor tag
         }
         __syncthreads();
     }
@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(SEL_THREADS) select_count_kernel(const TF *fla
 
 // Exclusive scan of the tile counts in place by one CTA (8 bytes per 8192
 // elements: 32768 counts = 256 KiB for 2^28 elements), total -> *total.  No look-back
-// descriptors, so the select scratch never needs epoch tags.
+// descriptors, so the select scratch never needs epoch tags.  Counts and offsets are
+// kept shifted left by 2: a scratch shared with a later scan then holds no word whose
+// status bits could pass for a published descriptor.
 constexpr int SEL_SCAN_THREADS = 1024;
 constexpr int SEL_SCAN_PER = 8;
 __global__ void __launch_bounds__(SEL_SCAN_THREADS) select_offsets_kernel(long long *counts, int64_t ntiles,
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(SEL_SCAN_THREADS) select_offsets_kernel(long l
         long long own = 0;
 #pragma unroll
         for (int j = 0; j < SEL_SCAN_PER; ++j) {
-            x[j] = i0 + j < ntiles ? counts[i0 + j] : 0;
+            x[j] = i0 + j < ntiles ? (counts[i0 + j] >> 2) : 0;
             own += x[j];
         }
         long long inc = own;
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(SEL_SCAN_THREADS) select_offsets_kernel(long l
         long long run = carry + wbase + inc - own;
 #pragma unroll
         for (int j = 0; j < SEL_SCAN_PER; ++j) {
-            if (i0 + j < ntiles) counts[i0 + j] = run;
+            if (i0 + j < ntiles) counts[i0 + j] = run << 2;
             run += x[j];
         }
         carry += btot;
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_scatter_kernel(const TV *v
     }
     __syncthreads();
 
-    const int64_t off = offsets[t];
+    const int64_t off = offsets[t] >> 2;
     for (int i = threadIdx.x; i < sel_tile; i += SEL_THREADS) out[off + i] = stage[i];
     if constexpr (PARTITION) {
         // rejected elements before this tile = t0 - off; all rejected follow the total

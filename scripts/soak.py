@@ -4,7 +4,8 @@
 
 Random dtype pairs, sizes (1 .. 2^27), unaligned views, inclusive/exclusive,
 seeds, forced kernels (look-back / L2 rounds / stream / auto), batched rows
-(both kernels), compaction, with and without stall injection.  Prints a line
+(both kernels, row tickets, short rows, per-row tile grids, seeds and totals),
+CSR segmented scans, compaction, with and without stall injection.  Prints a line
 per 100 cases and exits non-zero on the first mismatch (with its parameters)."""
 import sys
 import time
@@ -68,17 +69,41 @@ while time.time() < deadline:
     compare(out.cpu().numpy(), ref_scan(a[off:], dout, excl, seed),
             f"scan {din.__name__}->{dout.__name__} n={n} off={off} excl={excl} seed={seed} kernel={kern} stall={stall}")
     cases += 1
-    if cases % 7 == 0:  # batched rows
-        rows, cols = int(rng.integers(1, 700)), int(rng.integers(1, 40000))
+    if cases % 7 == 0:  # batched rows: both kernels, row tickets, short rows, per-row tile grids
+        rows = int(rng.choice([int(rng.integers(1, 700)), int(rng.integers(700, 20000))]))
+        cols = int(rng.choice([int(rng.integers(1, 40000)), int(rng.integers(1, 3000))]))
         b = rng.integers(0, 255, (rows, cols)).astype(np.int32)
-        lib.ps_set_tuning(b"rows_kernel", int(rng.integers(0, 3)))
+        knobs = {b"rows_kernel": int(rng.integers(0, 3)), b"rows_dynamic": int(rng.integers(0, 2)),
+                 b"rows_multi": int(rng.integers(0, 2)), b"tiles_row_lead": int(rng.integers(0, 2))}
+        saved = {k: lib.ps_get_tuning(k) for k in knobs}
+        for k, v in knobs.items():
+            lib.ps_set_tuning(k, v)
+        seeded = bool(rng.integers(2))
+        seeds = torch.arange(rows, dtype=torch.int64, device="cuda") * 5 if seeded else None
         o = torch.empty((rows, cols), dtype=torch.int64, device="cuda")
-        dev.scan_batched(torch.from_numpy(b).cuda(), o, exclusive=excl)
-        lib.ps_set_tuning(b"rows_kernel", 0)
-        want = np.cumsum(b, axis=1, dtype=np.int64)
+        tots = torch.empty(rows, dtype=torch.int64, device="cuda")
+        dev.scan_batched(torch.from_numpy(b).cuda(), o, exclusive=excl, row_seeds=seeds, row_totals=tots)
+        for k, v in saved.items():
+            lib.ps_set_tuning(k, v)
+        want = np.cumsum(b, axis=1, dtype=np.int64) + ((np.arange(rows) * 5)[:, None] if seeded else 0)
+        compare(tots.cpu().numpy(), want[:, -1], f"row totals {rows}x{cols} {knobs} seeded={seeded}")
         if excl:
             want = want - b
-        compare(o.cpu().numpy(), want, f"rows {rows}x{cols} excl={excl}")
+        compare(o.cpu().numpy(), want, f"rows {rows}x{cols} excl={excl} {knobs} seeded={seeded}")
+    if cases % 13 == 0:  # CSR segmented
+        m = int(rng.choice([1000, 1 << 20, 3_000_001]))
+        nseg = int(rng.choice([1, 10, 1000, m // 4 + 1]))
+        cuts = np.sort(rng.integers(0, m + 1, nseg - 1))
+        offs = np.concatenate([[0], cuts, [m]]).astype(np.int64)
+        v = rng.integers(0, 100, m).astype(np.int32)
+        o = torch.empty(m, dtype=torch.int64, device="cuda")
+        dev.scan_segmented(torch.from_numpy(v).cuda(), torch.from_numpy(offs).cuda(), o, exclusive=excl)
+        c = np.cumsum(v.astype(np.int64))
+        starts = np.repeat(offs[:-1], np.diff(offs))
+        want = c - np.where(starts > 0, c[np.maximum(starts - 1, 0)], 0)
+        if excl:
+            want = want - v
+        compare(o.cpu().numpy(), want, f"segmented m={m} nseg={nseg} excl={excl}")
     if cases % 11 == 0:  # compaction
         m = int(rng.choice([1000, 1 << 20, 5_000_000]))
         v = rng.integers(-1000, 1000, m).astype(np.int32)

@@ -553,6 +553,39 @@ def test_segmented_distributions(ps):
         np.testing.assert_allclose(_host(out), (c - before).astype(np.float32), rtol=1e-5, atol=1e-4, err_msg=name)
 
 
+def test_shared_scratch_segmented_then_stream(ps, force_kernel):
+    """One scratch shared by a segmented scan and a later stream-kernel scan (the
+    C ABI allows it): the segmented pre-pass's tile -> segment words sit where the
+    stream kernel's region descriptors go, and must never pass for a published
+    descriptor of a later epoch (segment 9 == (epoch 2 << 2) | 1 would, stored
+    plainly).  Integer ledgers poll early, so a stale match would be taken."""
+    from paper_2312_14874_b200 import _lib
+    lib = _lib.load()
+    force_kernel(3)
+    n = 1 << 24
+    r = np.random.default_rng(23)
+    x = _cuda(r.integers(0, 100, n, dtype=np.int32))
+    # a 100000-element segmented scan (13 tiles) puts its tile -> segment words at scratch
+    # offset 512, i.e. on region 0's descriptors of the stream kernel; segment 9 holds
+    # tiles 1..12, and 9 == (2 << 2) | 1 is a "published" tag for epoch 2
+    m = 100_000
+    offs = _cuda(np.concatenate([np.arange(10), [m]]).astype(np.int64))
+    sbytes = max(lib.ps_scan_segmented_scratch_bytes(m, 1, 2), lib.ps_scan_scratch_bytes(n, 1, 2))
+    for trial in range(3):
+        scratch = torch.zeros(sbytes, dtype=torch.uint8, device="cuda")
+        seg_out = torch.empty(m, dtype=torch.int64, device="cuda")
+        assert lib.ps_scan_segmented(x.data_ptr(), seg_out.data_ptr(), m, offs.data_ptr(), 10, 1, 2, 0, None,
+                                     scratch.data_ptr(), sbytes, 1, None) == 0
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        tot = torch.empty(1, dtype=torch.int64, device="cuda")
+        assert lib.ps_scan(x.data_ptr(), out.data_ptr(), n, 1, 2, 0, 0, None, 0, tot.data_ptr(),
+                           scratch.data_ptr(), sbytes, 2, None) == 0
+        torch.cuda.synchronize()
+        exp = np.cumsum(_host(x).astype(np.int64))
+        assert np.array_equal(_host(out), exp), trial
+        assert int(tot.item()) == int(exp[-1])
+
+
 def test_segmented(ps):
     from paper_2312_14874_b200 import device
     r = np.random.default_rng(9)
