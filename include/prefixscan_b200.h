@@ -36,7 +36,10 @@
  *   previous one (descriptors are epoch-tagged, so no per-call memset).  When
  *   the epochs run out, zero the buffer again and restart at 1.  (The first
  *   16 bytes of a batched scan's scratch are the rows kernel's row ticket;
- *   every launch leaves them at zero again.)
+ *   every launch leaves them at zero again.)  One scratch may serve every
+ *   entry point in turn: the non-descriptor words kernels leave in it
+ *   (segment and compaction bookkeeping) keep their two low bits 0, so they
+ *   never pass for a published descriptor of a later epoch.
  * - `in == out` (in place) is allowed; partial overlap is not.
  * - Return 0 on success, a PS_ERR_* (>0) on misuse, or a cudaError_t value
  *   offset by PS_ERR_CUDA_BASE on a CUDA failure.
