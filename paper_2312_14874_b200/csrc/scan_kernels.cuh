@@ -98,7 +98,10 @@ template <typename T> __device__ __forceinline__ V256 pack(const T *y) {
 }
 
 template <typename TIn, typename TOut, int WARPS, int ROWS>
-__global__ void __launch_bounds__(WARPS * 32)
+#ifndef PS_TILES_MINB
+#define PS_TILES_MINB 4  // 4 CTAs per SM (64 registers): more tiles in flight hide the look-back; 2, 3, 5, 6 and no bound were slower
+#endif
+__global__ void __launch_bounds__(WARPS * 32, PS_TILES_MINB)
     scan_tiles_kernel(const ScanArgs a) {
     using A = typename AccOf<TIn>::type;
     constexpr int VEC = 32 / sizeof(TIn);

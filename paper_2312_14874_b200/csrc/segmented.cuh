@@ -96,7 +96,7 @@ template <typename A> __device__ __forceinline__ Pair<A> combine(Pair<A> a, Pair
 }
 
 template <typename TIn, typename TOut, int WARPS, int ROWS>
-__global__ void __launch_bounds__(WARPS * 32) seg_scan_kernel(const SegArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, PS_TILES_MINB) seg_scan_kernel(const SegArgs a) {
     using A = typename AccOf<TIn>::type;
     constexpr int VEC = 32 / sizeof(TIn);
     constexpr int ROW_ELEMS = 32 * VEC;

@@ -5,6 +5,13 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
+import os  # noqa: E402
+
+from paper_2312_14874_b200 import _build  # noqa: E402
+
+if os.environ.get("LIB"):  # A/B against another build of the library
+    _build.LIB_PATH = os.environ["LIB"]
+    _build.up_to_date = lambda: True
 from paper_2312_14874_b200 import device  # noqa: E402
 
 PEAK = 6551.0
