@@ -8,7 +8,7 @@ C-ABI library instead of numba loops:
 reference (core.py)                here
 =================================  ==========================================
 sequential_inclusive_scan :118     one scan launch (ps_scan: stream kernel
-                                   >= 16 MiB, look-back kernel below)
+                                   >= 32 MiB, look-back kernel below)
 sequential_accumulate     :129     one deterministic reduction (ps_reduce)
 sequential_increment      :135     one vectorised add (ps_add_offset)
 exclusive_from_inclusive  :141     gather + tile shift (ps_shift_right)

@@ -78,7 +78,7 @@ bool overlaps_partially(const void *a, size_t abytes, const void *b, size_t bbyt
 struct Tuning {
     int scan_kernel = 0;                    // 0 auto, 1 look-back, 2 cache-partitioned rounds
     int64_t round_bytes = 0;                // input + output bytes per L2 region (0 = per-dtype default)
-    int64_t rounds_min_bytes = 16ll << 20;  // auto: rounds kernel from this many input bytes
+    int64_t rounds_min_bytes = 32ll << 20;  // auto: stream kernel from this many input bytes (scripts/crossover.py)
     int64_t round_lead = 2;                 // regions the reducer warps may run ahead of the scanners
     int64_t round_ramp = 0;                 // ramp regions at each end (sizes P/2^k .. P/2); 0 = off
     int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)

@@ -239,7 +239,7 @@ def test_every_algorithm_checksum_matches_oracle(device):
 @pytest.mark.parametrize("algo", GPU_ALGOS)
 @pytest.mark.parametrize("elem", ["i32", "f32"])
 def test_gpu_labels_large_device_resident(algo, elem):
-    # above the 16 MiB rounds threshold, so GPU-RND really runs the rounds kernel
+    # above the 32 MiB threshold of the large-input kernels
     rec = run_case(CaseConfig(algo=algo, elem_type=elem, n=(1 << 23) + 5, reps=5, seed=2,
                               device="cuda", out_of_place=True))
     assert rec.checksum == checksum(oracle_scan(make_input(elem, (1 << 23) + 5, 2)))
