@@ -98,7 +98,20 @@ class _Scratch:
         self.buf: torch.Tensor | None = None
         self.epoch = 0
 
-    def take(self, nbytes: int, n_epochs: int, device: torch.device) -> tuple[int, int, int]:
+    def take(self, nbytes: int, n_epochs: int, device: torch.device,
+             capturing: bool = False) -> tuple[int, int, int]:
+        if capturing:
+            # CUDA graph capture: the epoch is baked into the graph, so a replay would
+            # meet the descriptors of the previous replay under the same epoch.  The
+            # scratch is zeroed inside the graph instead (one memset node per launch),
+            # which makes every replay start from a clean scratch.
+            if self.buf is None or self.buf.numel() < nbytes:
+                raise RuntimeError("scan scratch must exist before CUDA graph capture: run the same call "
+                                   "once on the capture stream first (the usual warm-up)")
+            self.buf[:max(nbytes, 16)].zero_()
+            first = self.epoch + 1 if self.epoch + n_epochs <= _lib.PS_EPOCH_MAX else 1
+            self.epoch = first + n_epochs - 1
+            return self.buf.data_ptr(), self.buf.numel(), first
         if self.buf is None or self.buf.numel() < nbytes:
             size = max(nbytes, 1 << 16)
             if self.buf is not None:
@@ -126,7 +139,7 @@ def _scratch_for(device: torch.device, nbytes: int, n_epochs: int = 1, kind: str
         s = _scratch.get(key)
         if s is None:
             s = _scratch[key] = _Scratch()
-        return s.take(nbytes, n_epochs, device)
+        return s.take(nbytes, n_epochs, device, torch.cuda.is_current_stream_capturing())
 
 
 def _flat(t: torch.Tensor, name: str) -> torch.Tensor:

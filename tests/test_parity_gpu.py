@@ -781,3 +781,52 @@ def test_cfg5_full_properties(ps):
         w = x[a:a + (1 << 20)].cpu().numpy()
         carry = int(out[a - 1].item())
         assert np.array_equal(out[a:a + (1 << 20)].cpu().numpy(), np.cumsum(w) + carry)
+
+
+def test_cuda_graph_replays(ps):
+    """Scans captured in a CUDA graph and replayed several times over changing input
+    contents: every replay starts from a zeroed scratch (the epochs are baked into the
+    graph), so no replay can take a previous replay's descriptors for its own."""
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(29)
+    n_big, n_small = 9_000_011, 300_007
+    big = torch.empty(n_big, dtype=torch.int64, device="cuda")
+    small = torch.empty(n_small, dtype=torch.float32, device="cuda")
+    rows = torch.empty((3000, 5001), dtype=torch.int32, device="cuda")
+    flags = torch.empty(n_small, dtype=torch.int32, device="cuda")
+    ob, os_, orow = torch.empty_like(big), torch.empty_like(small), torch.empty((3000, 5001), dtype=torch.int64, device="cuda")
+    osel = torch.empty(n_small, dtype=torch.float32, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+
+    def work():
+        device.scan(big, ob)
+        device.scan(small, os_)
+        device.scan_batched(rows, orow, exclusive=True)
+        device.select(small, flags, osel, count=cnt)
+
+    with torch.cuda.stream(s):
+        work()  # warm-up: scratch sized on the capture stream
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        work()
+    for rep in range(4):
+        xb = r.integers(0, 1000, n_big, dtype=np.int64)
+        xs = r.random(n_small, dtype=np.float32)
+        xr = r.integers(0, 256, (3000, 5001), dtype=np.int32)
+        xf = r.integers(0, 2, n_small, dtype=np.int32)
+        big.copy_(torch.from_numpy(xb))
+        small.copy_(torch.from_numpy(xs))
+        rows.copy_(torch.from_numpy(xr))
+        flags.copy_(torch.from_numpy(xf))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(_host(ob), np.cumsum(xb)), rep
+        np.testing.assert_allclose(_host(os_), np.cumsum(xs.astype(np.float64)).astype(np.float32), rtol=1e-6)
+        inc = np.cumsum(xr.astype(np.int64), axis=1)
+        assert np.array_equal(_host(orow), inc - xr), rep
+        k = int(cnt.item())
+        assert k == int(xf.sum()) and np.array_equal(_host(osel)[:k], xs[xf != 0]), rep
