@@ -86,6 +86,25 @@ def test_batched_rows_under_stalls(rows_kernel):
     assert np.array_equal(out.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("cols,dynamic,multi", [(3000, 1, 1), (3000, 0, 1), (50_000, 1, 0), (20_000, 0, 0)])
+def test_rows_kernel_tickets_and_short_rows_under_stalls(cols, dynamic, multi):
+    """Row tickets (dynamic) and several short rows per buffer (multi) with the
+    producer / scanner hand-offs stalled at random: results exact, and the ticket
+    counters still return to zero (a second launch on the same scratch is exact)."""
+    from paper_2312_14874_b200 import device as dev
+    a = np.random.default_rng(17).integers(0, 256, (1500, cols), dtype=np.int32)
+    x = torch.from_numpy(a).cuda()
+    want = np.cumsum(a, axis=1, dtype=np.int64)
+    with tuning(rows_kernel=2, rows_dynamic=dynamic, rows_multi=multi):
+        for rep in range(2):
+            out = torch.empty(a.shape, dtype=torch.int64, device="cuda")
+            tots = torch.empty(a.shape[0], dtype=torch.int64, device="cuda")
+            with dev.stall_injection(seed=21 + rep, prob=0.2, max_ns=20000):
+                dev.scan_batched(x, out, row_totals=tots)
+            assert np.array_equal(out.cpu().numpy(), want), rep
+            assert np.array_equal(tots.cpu().numpy(), want[:, -1]), rep
+
+
 def test_stall_injection_restores_and_validates():
     from paper_2312_14874_b200 import _lib, device as dev
     lib = _lib.load()
