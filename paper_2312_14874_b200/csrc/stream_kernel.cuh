@@ -272,7 +272,10 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
 #endif
                 }
             }
-            named_sync(BAR_RED, RT);
+            // integer data: the reducer warps stay in step.  float data: warps 1.. go on
+            // to the next region while warp 0 publishes (tot[] of this buffer is not
+            // rewritten before the buffer comes round again; cfg2 +0.7 %, int -0.5 %)
+            if constexpr (!FLOAT) named_sync(BAR_RED, RT);
         }
         return;
     }
