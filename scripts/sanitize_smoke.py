@@ -48,6 +48,11 @@ for k in (1, 2):
     dev.scan_batched(x, o)
     check(o.cpu().numpy(), np.cumsum(rows, axis=1, dtype=np.int64), f"rows {k}")
 lib.ps_set_tuning(b"rows_kernel", 0)
+for shape in ((5000, 1000), (3000, 1001), (700, 250), (300, 20_001)):  # short rows, unaligned rows, uniform segments
+    b = r.integers(0, 255, shape, dtype=np.int32)
+    o = torch.empty(shape, dtype=torch.int64, device="cuda")
+    dev.scan_batched(torch.from_numpy(b).cuda(), o)
+    check(o.cpu().numpy(), np.cumsum(b, axis=1, dtype=np.int64), f"rows {shape}")
 x = torch.from_numpy(a64).cuda()
 check(int(dev.reduce(x).item()), int(a64.sum()), "reduce")
 dev.add_offset(x, 5)
@@ -66,5 +71,8 @@ dev.tree_down_sweep(t)
 check(t.cpu().numpy(), np.concatenate([[0], np.cumsum(a64[: 1 << 16])[:-1]]), "tree sweeps")
 offs = torch.tensor([0, 5, 100, 1000, 3_000_017], dtype=torch.int64, device="cuda")
 dev.scan_segmented(torch.from_numpy(a64).cuda(), offs)
+cuts = np.sort(r.integers(0, 3_000_018, 200_000))
+offs2 = torch.from_numpy(np.concatenate([[0], cuts, [3_000_017]]).astype(np.int64)).cuda()
+dev.scan_segmented(torch.from_numpy(a64).cuda(), offs2)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
