@@ -81,6 +81,9 @@ int main() {
     }
     if (getenv("F32GEO")) {  // float32 scanner/reducer geometry
         run<float, float, 8, 4, 6, 4>("f32 8x4 r4", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 8, 4, 6, 2>("f32 8x4 r2", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 8, 4, 6, 6>("f32 8x4 r6", in, out, N, scratch, epoch, 32 << 10);
+        run<float, float, 8, 4, 6, 8>("f32 8x4 r8", in, out, N, scratch, epoch, 32 << 10);
         run<float, float, 16, 2, 6, 4>("f32 16x2 r4", in, out, N, scratch, epoch, 32 << 10);
         run<float, float, 16, 2, 6, 8>("f32 16x2 r8", in, out, N, scratch, epoch, 32 << 10);
         run<float, float, 8, 2, 6, 4>("f32 8x2 r4", in, out, N, scratch, epoch, 32 << 10);
