@@ -16,7 +16,8 @@ def _rows(rows, cols, dt, seed):
 
 
 @pytest.mark.parametrize("rows,cols,chunk", [(1, 1, None), (3, 5, 2), (64, 1000, 7), (513, 4096, 100),
-                                             (2048, 2049, None)])
+                                             (2048, 2049, None), (20_000, 1000, None), (9000, 250, 3000),
+                                             (4000, 3001, None)])
 @pytest.mark.parametrize("exclusive", [False, True])
 def test_batched_host_int32_to_int64(rows, cols, chunk, exclusive):
     from paper_2312_14874_b200 import device as dev
