@@ -268,6 +268,8 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *                      multiple of 16 bytes): 1 = each row's tile grid starts on its own
  *                      32-byte boundary (vector accesses) and short contiguous rows
  *                      without seeds run as one uniform-segment scan; 0 = shared lead
+ *   "reduce_blocks"    ps_reduce: 1 = blocks of >= 256 KiB from a ticket (faster SMs
+ *                      take more; block partials folded in block order), 0 = grid-stride
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability

@@ -85,6 +85,7 @@ struct Tuning {
     int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
     int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
     int rows_dynamic = 1;                   // rows kernel: rows from a grid-wide ticket (0 = fixed shares)
+    int reduce_blocks = 1;                  // ps_reduce: blocks from a ticket (0 = grid-stride shares)
     int rows_multi = 1;                     // rows kernel: several short rows per buffer (0 = one row per buffer)
     int tiles_row_lead = 1;                 // look-back tiles, batched: 32-byte tile grid per row (0 = shared lead)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
@@ -671,6 +672,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "tiles_row_lead")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.tiles_row_lead = (int)value;
+    } else if (!std::strcmp(key, "reduce_blocks")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.reduce_blocks = (int)value;
     } else if (!std::strcmp(key, "rows_multi")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.rows_multi = (int)value;
@@ -717,6 +721,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "stream_inflight")) return g_tune.stream_inflight;
     if (!std::strcmp(key, "rows_dynamic")) return g_tune.rows_dynamic;
     if (!std::strcmp(key, "rows_multi")) return g_tune.rows_multi;
+    if (!std::strcmp(key, "reduce_blocks")) return g_tune.reduce_blocks;
     if (!std::strcmp(key, "tiles_row_lead")) return g_tune.tiles_row_lead;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
@@ -770,10 +775,12 @@ int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64
 #undef CALL
 }
 
+constexpr int64_t REDUCE_MAX_BLOCKS = 16384;  // block partials of reduce_blocks_kernel
+
 size_t ps_reduce_scratch_bytes(int64_t n, int dtype_in) {
     (void)n;
     if (!dsize(dtype_in)) return 0;
-    return 256 + 8 * 4096;  // ticket + up to 4096 CTA partials
+    return 256 + 8 * (REDUCE_MAX_BLOCKS + 64);  // tickets + block (or CTA) partials
 }
 
 int ps_reduce(const void *in, int64_t n, int dtype_in, uint64_t seed_bits, const void *seed_terms,
@@ -800,6 +807,18 @@ int ps_reduce(const void *in, int64_t n, int dtype_in, uint64_t seed_bits, const
     a.total = total_out;
     a.ticket = static_cast<uint32_t *>(scratch);
     a.partials = reinterpret_cast<uint64_t *>(static_cast<char *>(scratch) + 256);
+    a.blk_ticket = reinterpret_cast<unsigned long long *>(static_cast<char *>(scratch) + 8);
+    // blocks from a ticket (>= 256 KiB each, <= REDUCE_MAX_BLOCKS of them)
+    const int64_t nvec = n / vec;
+    int64_t bv = (int64_t)REDUCE_THREADS * 16;
+    if ((nvec + bv - 1) / bv > REDUCE_MAX_BLOCKS) bv = (nvec + REDUCE_MAX_BLOCKS - 1) / REDUCE_MAX_BLOCKS;
+    a.blk_vecs = bv;
+    if (g_tune.reduce_blocks && scratch_bytes >= 256 + 8 * (size_t)((nvec + bv - 1) / bv + 1)) {
+#define CALL(T) reduce_blocks_kernel<T, REDUCE_THREADS><<<(unsigned)grid, REDUCE_THREADS, 0, s>>>(a)
+        PS_DISPATCH_ONE(dtype_in, CALL);
+#undef CALL
+        return launch_rc();
+    }
 #define CALL(T) reduce_kernel<T, REDUCE_THREADS><<<(unsigned)grid, REDUCE_THREADS, 0, s>>>(a)
     PS_DISPATCH_ONE(dtype_in, CALL);
 #undef CALL

@@ -335,8 +335,10 @@ struct ReduceArgs {
     const void *seed_terms;
     int64_t n_seed_terms;
     void *total;            // acc-typed
-    uint64_t *partials;     // one per CTA
+    uint64_t *partials;     // one per CTA (reduce_kernel) or per block (reduce_blocks_kernel)
     uint32_t *ticket;       // zero between launches (the last CTA resets it)
+    unsigned long long *blk_ticket;  // reduce_blocks_kernel: next block, zero between launches
+    int64_t blk_vecs;       // reduce_blocks_kernel: 32-byte vectors per block
 };
 
 template <typename A, int THREADS> __device__ __forceinline__ A block_sum(A v, A *smem) {
@@ -413,6 +415,85 @@ __global__ void __launch_bounds__(THREADS) reduce_kernel(const ReduceArgs a) {
         }
         *reinterpret_cast<A *>(a.total) = seed + p;
         *a.ticket = 0;
+    }
+}
+
+// Blocks of blk_vecs vectors taken from a ticket (an SM that streams faster takes
+// more of them; fixed grid-stride shares leave the grid waiting for the slowest
+// SMs, scripts/sm_fairness.cu).  Each block's sum lands in partials[block] and
+// the last CTA folds them in block order, so float totals stay run-to-run
+// identical whichever CTA reduced which block.
+template <typename TIn, int THREADS>
+__global__ void __launch_bounds__(THREADS) reduce_blocks_kernel(const ReduceArgs a) {
+    using A = typename AccOf<TIn>::type;
+    constexpr int VEC = 32 / sizeof(TIn);
+    __shared__ A smem[THREADS / 32];
+    __shared__ int64_t s_blk;
+    __shared__ bool last;
+    const TIn *in = reinterpret_cast<const TIn *>(a.in);
+    const int64_t head = a.lead < a.n ? a.lead : a.n;
+    const int64_t nvec = (a.n - head) / VEC;
+    const int64_t tail0 = head + nvec * VEC;
+    const int64_t nblk = (nvec + a.blk_vecs - 1) / a.blk_vecs;
+    if (threadIdx.x == 0) s_blk = (int64_t)atomicAdd(a.blk_ticket, 1ull);
+    __syncthreads();
+    int64_t blk = s_blk;
+    while (blk < nblk) {
+        __syncthreads();  // everyone has read s_blk
+        if (threadIdx.x == 0) s_blk = (int64_t)atomicAdd(a.blk_ticket, 1ull);  // next one, in flight
+        const int64_t v0 = blk * a.blk_vecs;
+        const int64_t v1 = v0 + a.blk_vecs < nvec ? v0 + a.blk_vecs : nvec;
+        A acc = (A)0;
+        int64_t v = v0 + threadIdx.x;
+        for (; v + 3 * THREADS < v1; v += 4 * THREADS) {
+            V256 r0 = ldg256_stream(in + head + v * VEC);
+            V256 r1 = ldg256_stream(in + head + (v + THREADS) * VEC);
+            V256 r2 = ldg256_stream(in + head + (v + 2 * THREADS) * VEC);
+            V256 r3 = ldg256_stream(in + head + (v + 3 * THREADS) * VEC);
+            TIn x0[VEC], x1[VEC], x2[VEC], x3[VEC];
+            unpack<TIn>(r0, x0); unpack<TIn>(r1, x1); unpack<TIn>(r2, x2); unpack<TIn>(r3, x3);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc += (A)x0[j];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc += (A)x1[j];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc += (A)x2[j];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc += (A)x3[j];
+        }
+        for (; v < v1; v += THREADS) {
+            TIn x0[VEC];
+            unpack<TIn>(ldg256_stream(in + head + v * VEC), x0);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc += (A)x0[j];
+        }
+        const A bs = block_sum<A, THREADS>(acc, smem);  // ends with __syncthreads: s_blk is written
+        if (threadIdx.x == 0) st_relaxed_u64(a.partials + blk, acc_to_bits<A>(bs));
+        blk = s_blk;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t t = atomicAdd(a.ticket, 1u);
+        last = t == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // last CTA: the blocks in order, then the unaligned head and tail elements
+    A p = (A)0;
+    for (int64_t i = threadIdx.x; i < nblk; i += THREADS) p += acc_from_bits<A>(ld_relaxed_u64(a.partials + i));
+    if (threadIdx.x < head) p += (A)in[threadIdx.x];
+    if (threadIdx.x < a.n - tail0) p += (A)in[tail0 + threadIdx.x];
+    p = block_sum<A, THREADS>(p, smem);
+    if (threadIdx.x == 0) {
+        A seed = acc_from_bits<A>(a.seed_bits);
+        if (a.seed_terms) {
+            const A *st = reinterpret_cast<const A *>(a.seed_terms);
+            for (int64_t i = 0; i < a.n_seed_terms; ++i) seed += st[i];
+        }
+        *reinterpret_cast<A *>(a.total) = seed + p;
+        *a.ticket = 0;
+        *a.blk_ticket = 0;
     }
 }
 

@@ -830,3 +830,28 @@ def test_cuda_graph_replays(ps):
         assert np.array_equal(_host(orow), inc - xr), rep
         k = int(cnt.item())
         assert k == int(xf.sum()) and np.array_equal(_host(osel)[:k], xs[xf != 0]), rep
+
+
+@pytest.mark.parametrize("blocks", [0, 1])
+def test_reduce_block_tickets(ps, blocks):
+    """ps_reduce with blocks from a ticket (1) or grid-stride shares (0): exact for
+    integers, run-to-run identical for floats (blocks fold in block order whichever
+    CTA reduced them), unaligned heads and tails, seeds, repeated launches."""
+    from paper_2312_14874_b200 import _lib, device
+    lib = _lib.load()
+    saved = lib.ps_get_tuning(b"reduce_blocks")
+    lib.ps_set_tuning(b"reduce_blocks", blocks)
+    try:
+        r = np.random.default_rng(41)
+        for n, off in ((1, 0), (7, 3), (100_003, 1), (5_000_011, 5), (1 << 24, 0), ((1 << 26) + 3, 2)):
+            x = r.integers(-1000, 1000, n + off, dtype=np.int64)
+            t = _cuda(x)[off:]
+            for rep in range(2):
+                assert int(device.reduce(t, seed=7).item()) == int(x[off:].sum()) + 7, (n, off)
+            f = r.random(n + off, dtype=np.float32)
+            ft = _cuda(f)[off:]
+            a, b = float(device.reduce(ft).item()), float(device.reduce(ft).item())
+            assert a == b
+            np.testing.assert_allclose(a, f[off:].astype(np.float64).sum(), rtol=1e-9)
+    finally:
+        lib.ps_set_tuning(b"reduce_blocks", saved)
