@@ -270,6 +270,8 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *                      without seeds run as one uniform-segment scan; 0 = shared lead
  *   "reduce_blocks"    ps_reduce: 1 = blocks of >= 256 KiB from a ticket (faster SMs
  *                      take more; block partials folded in block order), 0 = grid-stride
+ *   "add_chunked"      ps_add_offset: 1 = one CTA per 64 KiB (hardware-balanced),
+ *                      0 = a grid of 8 CTAs per SM with grid-stride shares
  *   "stall_seed" / "stall_prob" / "stall_ns"
  *                      stress tests only: every role hand-off of the look-back,
  *                      rounds and rows kernels sleeps with probability

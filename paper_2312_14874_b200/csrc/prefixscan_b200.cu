@@ -86,6 +86,7 @@ struct Tuning {
     int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
     int rows_dynamic = 1;                   // rows kernel: rows from a grid-wide ticket (0 = fixed shares)
     int reduce_blocks = 1;                  // ps_reduce: blocks from a ticket (0 = grid-stride shares)
+    int add_chunked = 1;                    // ps_add_offset: one CTA per 64 KiB (0 = grid-stride shares)
     int rows_multi = 1;                     // rows kernel: several short rows per buffer (0 = one row per buffer)
     int tiles_row_lead = 1;                 // look-back tiles, batched: 32-byte tile grid per row (0 = shared lead)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
@@ -672,6 +673,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "tiles_row_lead")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.tiles_row_lead = (int)value;
+    } else if (!std::strcmp(key, "add_chunked")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.add_chunked = (int)value;
     } else if (!std::strcmp(key, "reduce_blocks")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.reduce_blocks = (int)value;
@@ -722,6 +726,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "rows_dynamic")) return g_tune.rows_dynamic;
     if (!std::strcmp(key, "rows_multi")) return g_tune.rows_multi;
     if (!std::strcmp(key, "reduce_blocks")) return g_tune.reduce_blocks;
+    if (!std::strcmp(key, "add_chunked")) return g_tune.add_chunked;
     if (!std::strcmp(key, "tiles_row_lead")) return g_tune.tiles_row_lead;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
@@ -839,6 +844,13 @@ int ps_add_offset(void *buf, int64_t n, int dtype, uint64_t delta_bits, const vo
     const int64_t vec = 32 / (int64_t)dsize(dtype);
     int64_t want = (n / vec + 255) / 256;
     int64_t grid = want < (int64_t)sms * 8 ? want : (int64_t)sms * 8;
+    if (g_tune.add_chunked) {
+        // one CTA per 2048 vectors (64 KiB): the hardware hands blocks to whichever SM
+        // is free, so faster SMs take more (grid-stride shares leave the grid waiting
+        // for the slowest SMs)
+        want = (n / vec + 2047) / 2048;
+        grid = want > 0x7fffffffLL ? 0x7fffffffLL : want;
+    }
     if (grid < 1) grid = 1;
 #define CALL(T)                                                                                          \
     add_offset_kernel<T><<<(unsigned)grid, 256, 0, s>>>(static_cast<T *>(buf), n, lead, delta_bits, delta_terms, \

@@ -142,7 +142,8 @@ def test_tuning_knobs_roundtrip(lib):
                            (b"rows_dynamic", 0, 2),
                            (b"rows_multi", 0, 2),
                            (b"tiles_row_lead", 0, 2),
-                           (b"reduce_blocks", 0, 2)):
+                           (b"reduce_blocks", 0, 2),
+                           (b"add_chunked", 0, 2)):
         prev = lib.ps_get_tuning(key)
         assert lib.ps_set_tuning(key, good) == 0 and lib.ps_get_tuning(key) == good
         assert lib.ps_set_tuning(key, bad) == _lib.PS_ERR_ARG and lib.ps_get_tuning(key) == good
