@@ -5,7 +5,8 @@
 Random dtype pairs, sizes (1 .. 2^27), unaligned views, inclusive/exclusive,
 seeds, forced kernels (look-back / L2 rounds / stream / auto), batched rows
 (both kernels, row tickets, short rows, per-row tile grids, seeds and totals),
-CSR segmented scans, compaction, with and without stall injection.  Prints a line
+CSR segmented scans, compaction, reduce and add-offset, with and without stall
+injection.  Prints a line
 per 100 cases and exits non-zero on the first mismatch (with its parameters)."""
 import sys
 import time
@@ -113,6 +114,18 @@ while time.time() < deadline:
         lib.ps_set_tuning(b"select_kernel", 0)
         k = int(cnt.item())
         compare(o[:k].cpu().numpy(), v[f != 0], f"select m={m}")
+    if cases % 5 == 0:  # reduce (block tickets) and add_offset (one CTA per 64 KiB)
+        m = int(rng.choice([1, 1000, 1 << 20, 9_000_011, 1 << 26]))
+        o2 = int(rng.integers(0, 8))
+        v = rng.integers(-1000, 1000, m + o2).astype(np.int64)
+        t = torch.from_numpy(v).cuda()[o2:]
+        lib.ps_set_tuning(b"reduce_blocks", int(rng.integers(0, 2)))
+        compare(np.array([int(dev.reduce(t).item())]), np.array([int(v[o2:].sum())]), f"reduce m={m} off={o2}")
+        lib.ps_set_tuning(b"reduce_blocks", 1)
+        lib.ps_set_tuning(b"add_chunked", int(rng.integers(0, 2)))
+        dev.add_offset(t, 17)
+        lib.ps_set_tuning(b"add_chunked", 1)
+        compare(t.cpu().numpy(), v[o2:] + 17, f"add_offset m={m} off={o2}")
     if cases % 100 == 0:
         print(f"{cases} cases ok", flush=True)
 print(f"soak ok: {cases} cases")
