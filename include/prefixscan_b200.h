@@ -160,14 +160,28 @@ size_t ps_scan_host_workspace_bytes(int64_t chunk_elems, int dtype_in, int dtype
 /* Number of epochs ps_scan_host consumes (one per chunk). */
 int64_t ps_scan_host_epochs(int64_t n, int64_t chunk_elems);
 
-/* End-to-end scan of HOST buffers (pinned for full speed): chunked pipeline of
- * H2D copy -> look-back scan seeded by the previous chunk's total -> D2H copy
- * over three CUDA streams.  Blocks until out_host and *total_host (acc-typed,
+/* End-to-end scan of HOST buffers: chunked pipeline of H2D copy -> scan
+ * seeded by the previous chunk's total -> D2H copy over three CUDA streams.
+ * Page-locked buffers are copied directly; pageable ones go through a ring of
+ * pinned bounce buffers filled and drained by host copy threads, overlapped
+ * with the transfers of neighbouring chunks (in == out allowed).  Blocks until out_host and *total_host (acc-typed,
  * host, nullable) are written.  Epochs epoch .. epoch+ps_scan_host_epochs-1
  * are used on the scratch inside `workspace` (zero-filled when allocated). */
 int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, int dtype_out,
                  int exclusive, uint64_t seed_bits, void *total_host, void *workspace,
                  size_t workspace_bytes, int64_t chunk_elems, uint32_t epoch, void *stream);
+
+/* Page-lock a caller-owned host range in place (cudaHostRegister) so that
+ * ps_scan_host / ps_scan_batched_host stream it at full PCIe rate without a
+ * copy into a pinned buffer -- the reference's users pass plain numpy arrays
+ * (core.py:118-126), which this turns into DMA-able memory.  *registered
+ * (nullable) = 1 if this call registered the range, 0 if it already was page-
+ * locked (nothing to undo).  ps_host_unregister undoes a registration;
+ * ps_host_is_pinned reports 1 for page-locked (registered or cudaHostAlloc)
+ * memory and 0 for pageable memory. */
+int ps_host_register(void *ptr, size_t bytes, int *registered);
+int ps_host_unregister(void *ptr);
+int ps_host_is_pinned(const void *ptr);
 
 /* Blelloch tree step functions on a power-of-two span, in place, element-typed
  * arithmetic in the reference's exact pairing (bit-identical float results):

@@ -78,38 +78,59 @@
         buf[0] = identity;                                                             \
         return last;                                                                   \
     }                                                                                  \
-    static A horizontal_##K(int w, const T *src, T *dst, int64_t start, int64_t len,   \
-                            A offset) {                                                \
-        A acc = offset;                                                                \
-        T v[16];                                                                       \
-        int64_t end = start + len, b = start;                                          \
-        while (b + w <= end) {                                                         \
-            for (int j = 0; j < w; ++j) v[j] = src[b + j];                             \
-            for (int sh = 1; sh < w; sh <<= 1)                                         \
-                for (int j = w - 1; j >= sh; --j) v[j] = (T)(v[j] + v[j - sh]);        \
-            for (int j = 0; j < w; ++j) dst[b + j] = CVT((A)v[j] + acc);               \
-            acc = acc + (A)v[w - 1];                                                   \
-            b += w;                                                                    \
-        }                                                                              \
-        for (int64_t i = b; i < end; ++i) {                                            \
-            acc = acc + (A)src[i];                                                     \
-            dst[i] = CVT(acc);                                                         \
-        }                                                                              \
-        return acc;                                                                    \
-    }                                                                                  \
-    static A simd_accumulate_##K(int w, const T *src, int64_t start, int64_t len) {    \
-        A part[16];                                                                    \
-        for (int j = 0; j < w; ++j) part[j] = (A)0;                                    \
-        int64_t end = start + len, b = start;                                          \
-        while (b + w <= end) {                                                         \
-            for (int j = 0; j < w; ++j) part[j] = part[j] + (A)src[b + j];             \
-            b += w;                                                                    \
-        }                                                                              \
-        A acc = (A)0;                                                                  \
-        for (int j = 0; j < w; ++j) acc = acc + part[j];                               \
-        for (int64_t i = b; i < end; ++i) acc = acc + (A)src[i];                       \
-        return acc;                                                                    \
-    }                                                                                  \
+    /* W is a compile-time lane count so gcc keeps the w-vector in registers  \
+     * and emits vector shifts/adds; the arithmetic (order, types) is the      \
+     * reference's, unchanged.  Dispatched from horizontal_##K below. */        \
+    static inline __attribute__((always_inline)) A horizontal_w_##K(           \
+        const int W, const T *src, T *dst, int64_t start, int64_t len,          \
+        A offset) {                                                             \
+        A acc = offset;                                                         \
+        T v[16];                                                                \
+        int64_t end = start + len, b = start;                                   \
+        while (b + W <= end) {                                                  \
+            for (int j = 0; j < W; ++j) v[j] = src[b + j];                      \
+            for (int sh = 1; sh < W; sh <<= 1)                                  \
+                for (int j = W - 1; j >= sh; --j) v[j] = (T)(v[j] + v[j - sh]); \
+            for (int j = 0; j < W; ++j) dst[b + j] = CVT((A)v[j] + acc);        \
+            acc = acc + (A)v[W - 1];                                            \
+            b += W;                                                             \
+        }                                                                       \
+        for (int64_t i = b; i < end; ++i) {                                     \
+            acc = acc + (A)src[i];                                              \
+            dst[i] = CVT(acc);                                                  \
+        }                                                                       \
+        return acc;                                                             \
+    }                                                                           \
+    static A horizontal_##K(int w, const T *src, T *dst, int64_t start,         \
+                            int64_t len, A offset) {                            \
+        switch (w) {                                                            \
+            case 4: return horizontal_w_##K(4, src, dst, start, len, offset);   \
+            case 8: return horizontal_w_##K(8, src, dst, start, len, offset);   \
+            default: return horizontal_w_##K(16, src, dst, start, len, offset); \
+        }                                                                       \
+    }                                                                           \
+    static inline __attribute__((always_inline)) A simd_accumulate_w_##K(      \
+        const int W, const T *src, int64_t start, int64_t len) {                \
+        A part[16];                                                             \
+        for (int j = 0; j < W; ++j) part[j] = (A)0;                             \
+        int64_t end = start + len, b = start;                                   \
+        while (b + W <= end) {                                                  \
+            for (int j = 0; j < W; ++j) part[j] = part[j] + (A)src[b + j];      \
+            b += W;                                                             \
+        }                                                                       \
+        A acc = (A)0;                                                           \
+        for (int j = 0; j < W; ++j) acc = acc + part[j];                        \
+        for (int64_t i = b; i < end; ++i) acc = acc + (A)src[i];                \
+        return acc;                                                             \
+    }                                                                           \
+    static A simd_accumulate_##K(int w, const T *src, int64_t start,            \
+                                 int64_t len) {                                 \
+        switch (w) {                                                            \
+            case 4: return simd_accumulate_w_##K(4, src, start, len);           \
+            case 8: return simd_accumulate_w_##K(8, src, start, len);           \
+            default: return simd_accumulate_w_##K(16, src, start, len);         \
+        }                                                                       \
+    }                                                                           \
     /* simd.py:164-175 _vertical_pass1_scan: lane-chunk scans, lane 0 seeded */         \
     static void vp1_scan_##K(T *data, int64_t start, int64_t k, int w, A carry,        \
                              A *totals) {                                              \

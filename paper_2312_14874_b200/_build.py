@@ -7,6 +7,7 @@ seconds and the .so travels with the repository snapshot to the GPU box.
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -18,7 +19,6 @@ LIB_NAME = "libprefixscan_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 
 SOURCES = ["prefixscan_b200.cu"]
-HEADERS = ["scan_device.cuh", "scan_kernels.cuh", "segmented.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,7 +36,9 @@ def nvcc() -> str:
 
 
 def _inputs():
-    files = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    """Every file the library is built from: a header edit must rebuild it."""
+    files = [os.path.join(CSRC, s) for s in SOURCES]
+    files += sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")))
     files.append(os.path.join(ROOT, "include", "prefixscan_b200.h"))
     return files
 

@@ -47,6 +47,9 @@ SIGNATURES = {
     "ps_scan_host": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _u64, _vp, _vp, _sz, _i64, _u32, _vp]),
     "ps_scan_batched_host_workspace_bytes": (_sz, [_i64, _i64, _i32, _i32]),
     "ps_scan_batched_host": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, _i32, _vp, _sz, _i64, _u32, _vp]),
+    "ps_host_register": (_i32, [_vp, _sz, ctypes.POINTER(_i32)]),
+    "ps_host_unregister": (_i32, [_vp]),
+    "ps_host_is_pinned": (_i32, [_vp]),
     "ps_tree_up_sweep": (_i32, [_vp, _i64, _i32, _vp, _vp]),
     "ps_tree_down_sweep": (_i32, [_vp, _i64, _i32, _vp]),
     "ps_publish_total": (_i32, [_vp, _vp, _i32, _i32, _u32, _u32, _vp, _vp, _vp]),

@@ -18,6 +18,7 @@
 #include "rows_kernel.cuh"
 #include "select_kernels.cuh"
 #include "select_stream.cuh"
+#include "host_pipeline.h"
 
 namespace ps {
 namespace {
@@ -515,39 +516,8 @@ int write_seed_only(int din, void *totals, int64_t count, uint64_t seed_bits, co
     return launch_rc();
 }
 
-// ---- host-buffer pipeline: per-device helper streams/events ---------------------------------
-constexpr int NSLOT = 3;
-struct HostPipe {
-    bool ready = false;
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t start = nullptr, h2d_done[NSLOT], comp_done[NSLOT], d2h_done[NSLOT], end_d2h = nullptr;
-};
-std::mutex g_pipe_mu;
-HostPipe g_pipes[64];
-
-int get_pipe(HostPipe **out) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return cuda_rc(e);
-    if (dev < 0 || dev >= 64) return PS_ERR_ARG;
-    std::lock_guard<std::mutex> g(g_pipe_mu);
-    HostPipe &p = g_pipes[dev];
-    if (!p.ready) {
-        if ((e = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking)) != cudaSuccess) return cuda_rc(e);
-        if ((e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking)) != cudaSuccess) return cuda_rc(e);
-        cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&p.end_d2h, cudaEventDisableTiming);
-        for (int i = 0; i < NSLOT; ++i) {
-            cudaEventCreateWithFlags(&p.h2d_done[i], cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&p.comp_done[i], cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&p.d2h_done[i], cudaEventDisableTiming);
-        }
-        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_rc(e);
-        p.ready = true;
-    }
-    *out = &p;
-    return PS_OK;
-}
+// ---- host-buffer pipeline (host_pipeline.h): device workspace layout ----------------------------
+constexpr int NSLOT = host::NSLOT;
 
 struct HostLayout {
     size_t in_slot, out_slot, scratch, total;  // byte sizes
@@ -980,52 +950,42 @@ int ps_scan_host(const void *in_host, void *out_host, int64_t n, int dtype_in, i
     if (!workspace || workspace_bytes < L.total) return PS_ERR_SCRATCH;
     cudaStream_t comp = static_cast<cudaStream_t>(stream);
     char *ws = static_cast<char *>(workspace);
-    void *carry = ws + L.off_carry;
+    // two carry slots by chunk parity: chunk k seeds from slot (k-1)&1 and writes
+    // its total to slot k&1, so no kernel reads the word another one writes
+    char *carry = ws + L.off_carry;
     void *scratch = ws + L.off_scratch;
     if (n == 0) {
         if (total_host) std::memcpy(total_host, &seed_bits, 8);
         return PS_OK;
     }
-    HostPipe *P = nullptr;
-    int rc = get_pipe(&P);
-    if (rc) return rc;
-    cudaError_t e;
-    // helper streams start after everything already queued on the caller stream
-    if ((e = cudaEventRecord(P->start, comp)) != cudaSuccess) return cuda_rc(e);
-    cudaStreamWaitEvent(P->h2d, P->start, 0);
-    cudaStreamWaitEvent(P->d2h, P->start, 0);
+    host::Pipe *P = nullptr;
+    if (host::pipe_for_current_device(&P)) return PS_ERR_CUDA_BASE + (int)cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> guard(P->mu);
+    cudaError_t e = P->init();
+    if (e != cudaSuccess) return cuda_rc(e);
     const size_t bi = dsize(dtype_in), bo = dsize(dtype_out);
-    for (int64_t k = 0; k < nchunks; ++k) {
-        const int slot = (int)(k % NSLOT);
+    auto chunk_of = [&](int64_t k) {
         const int64_t off = k * chunk_elems;
         const int64_t len = (n - off) < chunk_elems ? (n - off) : chunk_elems;
-        void *din = ws + L.off_in + slot * L.in_slot;
-        void *dout = ws + L.off_out + slot * L.out_slot;
-        if (k >= NSLOT) cudaStreamWaitEvent(P->h2d, P->d2h_done[slot], 0);
-        e = cudaMemcpyAsync(din, static_cast<const char *>(in_host) + off * bi, (size_t)len * bi,
-                            cudaMemcpyHostToDevice, P->h2d);
-        if (e != cudaSuccess) return cuda_rc(e);
-        cudaEventRecord(P->h2d_done[slot], P->h2d);
-        cudaStreamWaitEvent(comp, P->h2d_done[slot], 0);
-        rc = ps_scan(din, dout, len, dtype_in, dtype_out, exclusive, k == 0 ? seed_bits : 0,
-                     k == 0 ? nullptr : carry, k == 0 ? 0 : 1, carry, scratch, L.scratch, epoch + (uint32_t)k, comp);
-        if (rc) return rc;
-        cudaEventRecord(P->comp_done[slot], comp);
-        cudaStreamWaitEvent(P->d2h, P->comp_done[slot], 0);
-        e = cudaMemcpyAsync(static_cast<char *>(out_host) + off * bo, dout, (size_t)len * bo,
-                            cudaMemcpyDeviceToHost, P->d2h);
-        if (e != cudaSuccess) return cuda_rc(e);
-        cudaEventRecord(P->d2h_done[slot], P->d2h);
-    }
+        return host::Chunk{(size_t)off * bi, (size_t)len * bi, (size_t)off * bo, (size_t)len * bo};
+    };
+    auto launch = [&](int64_t k, char *din, char *dout) {
+        const int64_t off = k * chunk_elems;
+        const int64_t len = (n - off) < chunk_elems ? (n - off) : chunk_elems;
+        return ps_scan(din, dout, len, dtype_in, dtype_out, exclusive, k == 0 ? seed_bits : 0,
+                       k == 0 ? nullptr : carry + 8 * ((k - 1) & 1), k == 0 ? 0 : 1, carry + 8 * (k & 1), scratch,
+                       L.scratch, epoch + (uint32_t)k, comp);
+    };
+    int rc = host::run(*P, static_cast<const char *>(in_host), static_cast<char *>(out_host), nchunks,
+                       (size_t)chunk_elems * bi, (size_t)chunk_elems * bo, ws + L.off_in, ws + L.off_out, L.in_slot,
+                       L.out_slot, comp, chunk_of, launch, &e);
+    if (rc > 0) return rc;
+    if (rc < 0) return cuda_rc(e);
     if (total_host) {
-        e = cudaMemcpyAsync(total_host, carry, 8, cudaMemcpyDeviceToHost, comp);
+        e = cudaMemcpy(total_host, carry + 8 * ((nchunks - 1) & 1), 8, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_rc(e);
     }
-    // the caller stream owns the workspace again only after the last D2H
-    cudaEventRecord(P->end_d2h, P->d2h);
-    cudaStreamWaitEvent(comp, P->end_d2h, 0);
-    e = cudaStreamSynchronize(comp);
-    return cuda_rc(e);
+    return PS_OK;
 }
 
 
@@ -1067,42 +1027,49 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
     cudaStream_t comp = static_cast<cudaStream_t>(stream);
     char *ws = static_cast<char *>(workspace);
     void *scratch = ws + L.off_scratch;
-    HostPipe *P = nullptr;
-    int rc = get_pipe(&P);
-    if (rc) return rc;
-    cudaError_t e;
-    if ((e = cudaEventRecord(P->start, comp)) != cudaSuccess) return cuda_rc(e);
-    cudaStreamWaitEvent(P->h2d, P->start, 0);
-    cudaStreamWaitEvent(P->d2h, P->start, 0);
+    host::Pipe *P = nullptr;
+    if (host::pipe_for_current_device(&P)) return PS_ERR_CUDA_BASE + (int)cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> guard(P->mu);
+    cudaError_t e = P->init();
+    if (e != cudaSuccess) return cuda_rc(e);
     const size_t bi = dsize(dtype_in), bo = dsize(dtype_out);
-    for (int64_t k = 0; k < nchunks; ++k) {
-        const int slot = (int)(k % NSLOT);
-        const int64_t r0 = k * chunk_rows;
-        const int64_t nr = (rows - r0) < chunk_rows ? (rows - r0) : chunk_rows;
-        const size_t elems = (size_t)(nr * cols);
-        void *din = ws + L.off_in + slot * L.in_slot;
-        void *dout = ws + L.off_out + slot * L.out_slot;
-        if (k >= NSLOT) cudaStreamWaitEvent(P->h2d, P->d2h_done[slot], 0);
-        e = cudaMemcpyAsync(din, static_cast<const char *>(in_host) + (size_t)(r0 * cols) * bi, elems * bi,
-                            cudaMemcpyHostToDevice, P->h2d);
-        if (e != cudaSuccess) return cuda_rc(e);
-        cudaEventRecord(P->h2d_done[slot], P->h2d);
-        cudaStreamWaitEvent(comp, P->h2d_done[slot], 0);
-        rc = ps_scan_batched(din, dout, nr, cols, cols, cols, dtype_in, dtype_out, exclusive, nullptr, nullptr,
-                             scratch, L.scratch, epoch + (uint32_t)k, comp);
-        if (rc) return rc;
-        cudaEventRecord(P->comp_done[slot], comp);
-        cudaStreamWaitEvent(P->d2h, P->comp_done[slot], 0);
-        e = cudaMemcpyAsync(static_cast<char *>(out_host) + (size_t)(r0 * cols) * bo, dout, elems * bo,
-                            cudaMemcpyDeviceToHost, P->d2h);
-        if (e != cudaSuccess) return cuda_rc(e);
-        cudaEventRecord(P->d2h_done[slot], P->d2h);
-    }
-    cudaEventRecord(P->end_d2h, P->d2h);
-    cudaStreamWaitEvent(comp, P->end_d2h, 0);
-    e = cudaStreamSynchronize(comp);
-    return cuda_rc(e);
+    auto rows_of = [&](int64_t k) { return (rows - k * chunk_rows) < chunk_rows ? (rows - k * chunk_rows) : chunk_rows; };
+    auto chunk_of = [&](int64_t k) {
+        const size_t e0 = (size_t)(k * chunk_rows * cols), elems = (size_t)(rows_of(k) * cols);
+        return host::Chunk{e0 * bi, elems * bi, e0 * bo, elems * bo};
+    };
+    auto launch = [&](int64_t k, char *din, char *dout) {
+        return ps_scan_batched(din, dout, rows_of(k), cols, cols, cols, dtype_in, dtype_out, exclusive, nullptr,
+                               nullptr, scratch, L.scratch, epoch + (uint32_t)k, comp);
+    };
+    int rc = host::run(*P, static_cast<const char *>(in_host), static_cast<char *>(out_host), nchunks,
+                       (size_t)(chunk_rows * cols) * bi, (size_t)(chunk_rows * cols) * bo, ws + L.off_in,
+                       ws + L.off_out, L.in_slot, L.out_slot, comp, chunk_of, launch, &e);
+    if (rc > 0) return rc;
+    if (rc < 0) return cuda_rc(e);
+    return PS_OK;
 }
+
+int ps_host_register(void *ptr, size_t bytes, int *registered) {
+    if (registered) *registered = 0;
+    if (!ptr || bytes == 0) return PS_OK;
+    if (host::is_pinned(ptr, bytes)) return PS_OK;
+    cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+        return PS_OK;
+    }
+    if (e != cudaSuccess) return cuda_rc(e);
+    if (registered) *registered = 1;
+    return PS_OK;
+}
+
+int ps_host_unregister(void *ptr) {
+    if (!ptr) return PS_OK;
+    return cuda_rc(cudaHostUnregister(ptr));
+}
+
+int ps_host_is_pinned(const void *ptr) { return host::is_pinned(ptr, 1) ? 1 : 0; }
 
 // ---- Blelloch tree step functions (simd.py:327-367) -------------------------------------------
 int ps_tree_up_sweep(void *data, int64_t n, int dtype, void *root_out, void *stream) {

@@ -97,6 +97,10 @@ class _Scratch:
     def __init__(self):
         self.buf: torch.Tensor | None = None
         self.epoch = 0
+        # buffers a captured CUDA graph may still address: never returned to the
+        # allocator, since every replay memsets and writes descriptors into them
+        self.captured = False
+        self.retired: list[torch.Tensor] = []
 
     def take(self, nbytes: int, n_epochs: int, device: torch.device,
              capturing: bool = False) -> tuple[int, int, int]:
@@ -108,6 +112,7 @@ class _Scratch:
             if self.buf is None or self.buf.numel() < nbytes:
                 raise RuntimeError("scan scratch must exist before CUDA graph capture: run the same call "
                                    "once on the capture stream first (the usual warm-up)")
+            self.captured = True
             self.buf[:max(nbytes, 16)].zero_()
             first = self.epoch + 1 if self.epoch + n_epochs <= _lib.PS_EPOCH_MAX else 1
             self.epoch = first + n_epochs - 1
@@ -116,6 +121,8 @@ class _Scratch:
             size = max(nbytes, 1 << 16)
             if self.buf is not None:
                 size = max(size, 2 * self.buf.numel())
+                if self.captured:
+                    self.retired.append(self.buf)
             self.buf = torch.zeros(size, dtype=torch.uint8, device=device)
             self.epoch = 0
         if self.epoch + n_epochs > _lib.PS_EPOCH_MAX:
@@ -424,7 +431,10 @@ def scan_segmented(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | N
     _require_cuda(x, "x")
     _flat(x, "x")
     out = x if out is None else out
+    _require_cuda(out, "out")
     _flat(out, "out")
+    if out.shape != x.shape:
+        raise ValueError("output buffer must match input shape")
     if offsets.dtype != torch.int64 or offsets.dim() != 1 or not offsets.is_cuda or not offsets.is_contiguous():
         raise ValueError("offsets must be a contiguous 1-D int64 CUDA tensor")
     nseg = offsets.numel() - 1
@@ -432,8 +442,12 @@ def scan_segmented(x: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | N
         raise ValueError("offsets needs at least one entry")
     ci, co = dtype_code(x.dtype), dtype_code(out.dtype)
     lib = _lib.load()
-    if seg_totals is not None and (seg_totals.dtype != _ACC_TORCH[ci] or seg_totals.numel() != nseg):
-        raise ValueError(f"seg_totals must be {_ACC_TORCH[ci]} with {nseg} entries")
+    if not _pair_ok(lib, ci, co):
+        raise ValueError(f"unsupported dtype pair {x.dtype} -> {out.dtype}")
+    if seg_totals is not None:
+        _require_cuda(seg_totals, "seg_totals")
+        if seg_totals.dtype != _ACC_TORCH[ci] or seg_totals.numel() != nseg or not seg_totals.is_contiguous():
+            raise ValueError(f"seg_totals must be a contiguous {_ACC_TORCH[ci]} tensor with {nseg} entries")
     sptr, sbytes, epoch = _scratch_for(x.device, lib.ps_scan_segmented_scratch_bytes(x.numel(), ci, co))
     rc = lib.ps_scan_segmented(_ptr(x), _ptr(out), x.numel(), _ptr(offsets), nseg, ci, co, int(bool(exclusive)),
                                _ptr(seg_totals), sptr, sbytes, epoch, _stream_ptr(x.device))
@@ -483,6 +497,67 @@ class _HostWorkspace:
 
 
 _host_ws: dict[int, _HostWorkspace] = {}
+# one host pipeline at a time per device: the workspace (slots + scratch) and the
+# library's per-device streams/bounce buffers are shared by every caller thread
+_host_locks: dict[int, threading.Lock] = {}
+_host_locks_guard = threading.Lock()
+
+
+def _host_lock(index: int) -> threading.Lock:
+    with _host_locks_guard:
+        lk = _host_locks.get(index)
+        if lk is None:
+            lk = _host_locks[index] = threading.Lock()
+        return lk
+
+
+def _host_range(a) -> tuple[int, int]:
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("pinned_host needs C-contiguous arrays")
+        return a.ctypes.data, a.nbytes
+    if isinstance(a, torch.Tensor) and not a.is_cuda:
+        if not a.is_contiguous():
+            raise ValueError("pinned_host needs contiguous tensors")
+        return a.data_ptr(), a.numel() * a.element_size()
+    raise ValueError("pinned_host takes host numpy arrays or CPU tensors")
+
+
+class pinned_host:
+    """Context manager: page-lock caller-owned host arrays in place
+    (cudaHostRegister through ``ps_host_register``) so the host pipelines DMA
+    them directly at full PCIe rate; unregisters on exit what it registered.
+    Arrays that are already page-locked are left alone."""
+
+    def __init__(self, *arrays):
+        self.ranges = [_host_range(a) for a in arrays if a is not None]
+        self.done: list[int] = []
+
+    def __enter__(self):
+        lib = _lib.load()
+        try:
+            for ptr, nbytes in self.ranges:
+                if nbytes == 0 or ptr in self.done:
+                    continue
+                flag = ctypes.c_int(0)
+                _lib.check(lib.ps_host_register(ptr, nbytes, ctypes.byref(flag)), "ps_host_register")
+                if flag.value:
+                    self.done.append(ptr)
+        except Exception:
+            self.__exit__(None, None, None)
+            raise
+        return self
+
+    def __exit__(self, *exc):
+        lib = _lib.load()
+        while self.done:
+            lib.ps_host_unregister(self.done.pop())
+
+
+def is_pinned(a) -> bool:
+    """True if the host array's memory is page-locked."""
+    ptr, _ = _host_range(a)
+    return bool(_lib.load().ps_host_is_pinned(ptr))
 
 
 def _host_pointer(a) -> tuple[int, int, int]:
@@ -501,9 +576,12 @@ def _host_pointer(a) -> tuple[int, int, int]:
 def scan_host(x, out=None, *, exclusive: bool = False, seed=0, chunk_elems: int | None = None,
               device: torch.device | int | None = None):
     """Scan HOST memory end to end (H2D -> scan -> D2H, pipelined in
-    chunks over three streams).  ``out`` defaults to ``x`` (in place).  Pinned
-    host memory gives full PCIe overlap; pageable memory works but serialises.
-    Blocks; returns the accumulator-precision total as a Python number."""
+    chunks over three streams).  ``out`` defaults to ``x`` (in place).
+    Page-locked memory is DMA'd directly; pageable memory (a plain numpy
+    array) is staged through the library's pinned bounce ring by host copy
+    threads, overlapped with the transfers.  Thread-safe (one pipeline per
+    device at a time).  Blocks; returns the accumulator-precision total as a
+    Python number."""
     xp, n, ci = _host_pointer(x)
     out = x if out is None else out
     op, n2, co = _host_pointer(out)
@@ -522,7 +600,7 @@ def scan_host(x, out=None, *, exclusive: bool = False, seed=0, chunk_elems: int 
         chunk_elems = max(want // eb, 1 << 16)
     wsb = lib.ps_scan_host_workspace_bytes(chunk_elems, ci, co)
     nep = lib.ps_scan_host_epochs(n, chunk_elems)
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev), _host_lock(dev.index):
         ws = _host_ws.setdefault(dev.index, _HostWorkspace())
         epoch = ws.take(wsb, nep, ("1d", chunk_elems, ci, co), dev)
         tot = np.zeros(1, np.uint64)
@@ -564,7 +642,7 @@ def scan_batched_host(x, out=None, *, exclusive: bool = False, chunk_rows: int |
     chunk_rows = min(chunk_rows, rows)
     wsb = lib.ps_scan_batched_host_workspace_bytes(chunk_rows, cols, ci, co)
     nep = lib.ps_scan_host_epochs(rows, chunk_rows)
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev), _host_lock(dev.index):
         ws = _host_ws.setdefault(dev.index, _HostWorkspace())
         epoch = ws.take(wsb, nep, ("rows", chunk_rows, cols, ci, co), dev)
         rc = lib.ps_scan_batched_host(xp, op, rows, cols, ci, co, int(bool(exclusive)), ws.buf.data_ptr(),

@@ -287,7 +287,7 @@ def test_bench_falls_back_to_nccl_when_p2p_is_unavailable():
                 raise RuntimeError("no symmetric memory here")
             self.exchange = exchange
 
-    obj, label = bench._make_sharded(Fake, SchemeId.ACCUMULATE_SCAN_EQUAL, "p2p", world=4)
+    obj, label = bench.make_sharded(SchemeId.ACCUMULATE_SCAN_EQUAL, "p2p", 4, cls=Fake)
     assert obj.exchange == "nccl" and label.startswith("nccl (p2p unavailable")
-    obj, label = bench._make_sharded(Fake, SchemeId.ACCUMULATE_SCAN_EQUAL, "nccl", world=4)
+    obj, label = bench.make_sharded(SchemeId.ACCUMULATE_SCAN_EQUAL, "nccl", 4, cls=Fake)
     assert label == "nccl"
