@@ -370,7 +370,7 @@ def make_inputs(cfg, world, rank, scaling, dev_t, dist):
         return _device_draw(cfg, shape, rank, dev_t), None, (rank * cfg["n"], cfg["n"])
     # strong: rank 0 draws the whole input once and sends every rank its EQUAL shard
     units = rows if rows else cfg["n"]
-    spans = equal_shards(units, world, align=1 if rows else max(1, 32 // esize))
+    spans = [(sp.start, sp.len) for sp in equal_shards(units, world, align=1 if rows else max(1, 32 // esize))]
     lo, ln = spans[rank]
     tdt = {"int64": torch.int64, "int32": torch.int32, "float32": torch.float32}[cfg["din"]]
     shape = (ln, cfg["cols"]) if rows else (ln,)

@@ -199,8 +199,9 @@ int ps_tree_down_sweep(void *data, int64_t n, int dtype, void *stream);
  * symmetric memory); slot (e & 1) * n_peers + h holds rank h's total of
  * exchange epoch e.  This call stores {epoch, *total} (device, acc-typed 8
  * bytes) into that slot of every peer's mailbox -- peer_mailboxes is a DEVICE
- * array of n_peers mapped base addresses -- with one system-scope 16-byte
- * store per peer, after waiting (in the kernel) until all n_peers totals of
+ * array of n_peers mapped base addresses -- as value store then flag store
+ * with st.release.sys (the consumer polls the flag with ld.acquire.sys and only
+ * then reads the value), after waiting (in the kernel) until all n_peers totals of
  * prev_epoch (0 = none) have arrived in own_mailbox, which guarantees no
  * slot is overwritten while a slower rank can still read it.  Stream-ordered
  * after the kernel that produced *total; a wait longer than ~10 s sets

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <immintrin.h>
 #include <cstdint>
 #include <cstring>
 #include <deque>
@@ -31,6 +32,43 @@ namespace host {
 
 constexpr int NSLOT = 3;                 // device (and bounce) slots in flight
 constexpr size_t COPY_PIECE = 1u << 20;  // host memcpy granularity across the pool
+
+// Host copy with streaming (non-temporal) stores: the destination -- a bounce
+// slot the DMA engine reads next, or the caller's output array -- is not read
+// back by this thread, so writing around the caches saves the read-for-
+// ownership of every destination line (a third of the host memory traffic of
+// a plain memcpy).  The staging path is bound by host memory bandwidth
+// (profiles/r02_e2e.md), so this is its main lever.
+__attribute__((target("avx2"))) inline void stream_copy_avx2(char *dst, const char *src, size_t n) {
+    const size_t head = (32 - ((uintptr_t)dst & 31)) & 31;
+    if (n < head + 256) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::memcpy(dst, src, head);
+    dst += head, src += head, n -= head;
+    size_t i = 0;
+    for (; i + 128 <= n; i += 128) {
+        __m256i a = _mm256_loadu_si256((const __m256i *)(src + i));
+        __m256i b = _mm256_loadu_si256((const __m256i *)(src + i + 32));
+        __m256i c = _mm256_loadu_si256((const __m256i *)(src + i + 64));
+        __m256i d = _mm256_loadu_si256((const __m256i *)(src + i + 96));
+        _mm256_stream_si256((__m256i *)(dst + i), a);
+        _mm256_stream_si256((__m256i *)(dst + i + 32), b);
+        _mm256_stream_si256((__m256i *)(dst + i + 64), c);
+        _mm256_stream_si256((__m256i *)(dst + i + 96), d);
+    }
+    _mm_sfence();
+    std::memcpy(dst + i, src + i, n - i);
+}
+
+inline void host_copy(char *dst, const char *src, size_t n) {
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    if (avx2)
+        stream_copy_avx2(dst, src, n);
+    else
+        std::memcpy(dst, src, n);
+}
 
 // A batch of host copies; `left` counts its unfinished pieces.
 struct CopyBatch {
@@ -107,7 +145,7 @@ class CopyPool {
     }
 
     void run(const Piece &p) {
-        std::memcpy(p.dst, p.src, p.bytes);
+        host_copy(p.dst, p.src, p.bytes);
         if (p.batch->left.fetch_sub(1, std::memory_order_acq_rel) == 1) {
             std::lock_guard<std::mutex> g(mu_);  // pairs with the predicate check in wait()
             done_cv_.notify_all();

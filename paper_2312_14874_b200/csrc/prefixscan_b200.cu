@@ -454,7 +454,7 @@ __global__ void publish_total_kernel(const uint64_t *total, ulonglong2 *const *p
     __syncthreads();
     const int h = threadIdx.x;
     if (h < n_peers)
-        st_desc_sys(peer_mailboxes[h] + (size_t)(epoch & 1) * n_peers + rank, ((uint64_t)epoch << 2) | ST_A, *total);
+        mailbox_post(peer_mailboxes[h] + (size_t)(epoch & 1) * n_peers + rank, epoch, *total);
 }
 
 template <typename A> __global__ void mailbox_seed_kernel(A *total, uint64_t seed_bits, Mailbox m) {

@@ -147,12 +147,20 @@ __device__ __forceinline__ void stall_site(const Stall &s, uint64_t a, uint64_t 
 }
 
 // ---- cross-GPU mailbox (fused exchange of shard totals over NVLink) ----------------------
-// Rank h's reduce publishes {epoch<<2 | 1, total bits} into slot h of every
-// peer's mailbox with one 16-byte system-scope store (ps_publish_total); a scan
-// that needs the carry of ranks 0..n-1 polls its own mailbox slots 0..n-1
-// from inside the kernel (only the warp that folds the seed waits; loads and
-// reductions of the first regions proceed meanwhile).  A wait that exceeds
-// ~10 s gives up and raises *timeout instead of hanging the GPU.
+// Rank h's reduce publishes its total into slot h of every peer's mailbox
+// (ps_publish_total); a scan that needs the carry of ranks 0..n-1 polls its
+// own mailbox slots 0..n-1 from inside the kernel (only the warp that folds
+// the seed waits; loads and reductions of the first regions proceed
+// meanwhile).  A wait that exceeds ~10 s gives up and raises *timeout
+// instead of hanging the GPU.
+//
+// Slot = 16 bytes {flag, value}.  Message passing in the PTX memory model at
+// system scope (the writer is another GPU across NVLink / NVSwitch): the
+// producer stores the value, then the flag word {epoch << 2 | 1} with
+// st.release.sys; the consumer polls the flag with ld.acquire.sys and reads the
+// value only after the flag matched.  Release/acquire orders the value before
+// the flag across devices; nothing relies on a 16-byte store being single-copy
+// atomic over the fabric.
 struct Mailbox {
     const ulonglong2 *slots;  // this GPU's mailbox (written by peers)
     int n;                    // slots to wait for (the ranks before this one)
@@ -164,15 +172,33 @@ __device__ __forceinline__ uint64_t global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ ulonglong2 ld_desc_sys(const ulonglong2 *p) {
-    ulonglong2 v;
-    asm volatile("{ .reg .b128 t; ld.relaxed.sys.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
-                 : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+__device__ __forceinline__ uint64_t ld_acquire_sys(const unsigned long long *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_desc_sys(ulonglong2 *p, uint64_t word, uint64_t value) {
-    asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.sys.global.b128 [%0], t; }"
-                 ::"l"(p), "l"(word), "l"(value) : "memory");
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const unsigned long long *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// producer side: value first, then the flag that makes it visible
+__device__ __forceinline__ void mailbox_post(ulonglong2 *slot, uint32_t epoch, uint64_t value) {
+    st_relaxed_sys(&slot->y, value);
+    st_release_sys(&slot->x, ((uint64_t)epoch << 2) | 1ull);
+}
+// consumer side: true (and *value) once the slot carries `epoch`
+__device__ __forceinline__ bool mailbox_try(const ulonglong2 *slot, uint32_t epoch, uint64_t *value) {
+    const uint64_t f = ld_acquire_sys(&slot->x);
+    if ((f & ~3ull) != ((uint64_t)epoch << 2) || (f & 3ull) == 0) return false;
+    *value = ld_relaxed_sys(&slot->y);
+    return true;
 }
 
 __device__ __forceinline__ void publish(const Desc &d, int64_t tile, uint32_t epoch, uint64_t st, uint64_t bits) {

@@ -24,23 +24,21 @@ namespace ps {
 template <typename A>
 __device__ A mailbox_sum(const Mailbox &m, int lane) {
     A v = (A)0;
-    const uint64_t want = (uint64_t)m.epoch << 2;
     for (int j = lane; j < m.n; j += 32) {
-        ulonglong2 d = ld_desc_sys(m.slots + j);
-        if ((d.x & ~3ull) != want || (d.x & 3ull) == 0) {
+        uint64_t bits = 0;
+        if (!mailbox_try(m.slots + j, m.epoch, &bits)) {
             const uint64_t t0 = global_ns();
             while (true) {
                 __nanosleep(100);
-                d = ld_desc_sys(m.slots + j);
-                if ((d.x & ~3ull) == want && (d.x & 3ull) != 0) break;
+                if (mailbox_try(m.slots + j, m.epoch, &bits)) break;
                 if (global_ns() - t0 > 10000000000ull) {
                     if (m.timeout) atomicExch(m.timeout, 1);
-                    d.y = 0;
+                    bits = 0;
                     break;
                 }
             }
         }
-        v += acc_from_bits<A>(d.y);
+        v += acc_from_bits<A>(bits);
     }
     return warp_sum(v);
 }
