@@ -292,6 +292,12 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *                      rounds and rows kernels sleeps with probability
  *                      stall_prob/1024 for a hashed time in [0, stall_ns)
  *                      (stall_ns 0 = off; the reference's delay_hook, engine.py:91)
+ *   "float_exact"      stream kernel, float32 -> float32: 0 = in-chunk scans in float32
+ *                      with the float64 carry applied as a float pair (FP32 pipe only,
+ *                      <= 1e-6 relative to float32(cumsum(float64))), 1 = float64 per
+ *                      element (bit-exact whenever the float64 sums are exact) (default 0)
+ * Knobs are per calling host thread: setting one never changes what another
+ * thread's calls launch.
  * Returns PS_ERR_ARG for an unknown key or value. */
 int ps_set_tuning(const char *key, int64_t value);
 int64_t ps_get_tuning(const char *key); /* -1 for an unknown key */

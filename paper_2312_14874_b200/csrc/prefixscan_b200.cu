@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/prefixscan_b200.h"
 #include "scan_kernels.cuh"
@@ -90,9 +91,13 @@ struct Tuning {
     int add_chunked = 1;                    // ps_add_offset: one CTA per 64 KiB (0 = grid-stride shares)
     int rows_multi = 1;                     // rows kernel: several short rows per buffer (0 = one row per buffer)
     int tiles_row_lead = 1;                 // look-back tiles, batched: 32-byte tile grid per row (0 = shared lead)
+    int float_exact = 0;                    // stream kernel float32 -> float32: 1 = float64 per element (bit-exact
+                                            // to float32(cumsum(float64)) whenever the float64 sums are exact)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
 };
-Tuning g_tune;
+// Per calling thread: a knob set by one host thread (a harness label, a stress
+// test's stall injection) never changes the kernels another thread launches.
+thread_local Tuning g_tune;
 
 // rounds kernel: scanner warps, rows per warp, TMA stages, reducer warps, reducer lead (regions)
 constexpr int RW = 8, RR = 4, RRED = 4;
@@ -222,10 +227,26 @@ int launch_rounds(const void *in, void *out, int64_t n, int64_t lead, int exclus
 // ---- shared-memory-resident streaming kernel (stream_kernel.cuh) ---------------------------------
 // measured with scripts/stream_variants.cu: six 32 KiB buffers per SM (regions of
 // 4.6 MiB) hide the grid-wide ledger exchange; three 64 KiB buffers do not
-constexpr int SSW = 8, SROWS = 4, SNBUF = 6, SRWP = 4;
+#ifndef PS_SNBUF
+#define PS_SNBUF 7
+#endif
+#ifndef PS_SRWP
+#define PS_SRWP 4
+#endif
+#ifndef PS_SSW
+#define PS_SSW 8
+#endif
+#ifndef PS_SROWS
+#define PS_SROWS 4
+#endif
+constexpr int SSW = PS_SSW, SROWS = PS_SROWS, SNBUF = PS_SNBUF, SRWP = PS_SRWP;
 #define SGEO StreamGeom<TIn, SSW, SROWS, SNBUF, SRWP>
 #define SKERN scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP>
 #define SKERN_STALL scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP, true>
+// float32 -> float32 with FP32-pipe arithmetic (stream_kernel.cuh f32pair_*); the
+// float64-per-element form stays selectable (tuning "float_exact" = 1)
+#define SKERN_F32 scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP, false, 1, true>
+#define SKERN_F32_STALL scan_stream_kernel<TIn, TOut, SSW, SROWS, SNBUF, SRWP, true, 1, true>
 
 constexpr int STREAM_MAX_GRID = 32 * GATHER_LP;  // the ledger warp gathers <= 5 descriptors per lane
 
@@ -284,6 +305,19 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
         kern = (const void *)SKERN_STALL;
         cudaFuncSetAttribute(SKERN_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, SGEO::smem(P));
+    }
+    if constexpr (std::is_same<TIn, float>::value && std::is_same<TOut, float>::value) {
+        if (!g_tune.float_exact) {
+            kern = a.stall.max_ns ? (const void *)SKERN_F32_STALL : (const void *)SKERN_F32;
+            static bool attr[64] = {false};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev >= 0 && dev < 64 && !attr[dev]) {
+                cudaFuncSetAttribute(SKERN_F32, cudaFuncAttributeMaxDynamicSharedMemorySize, SGEO::smem(P));
+                cudaFuncSetAttribute(SKERN_F32_STALL, cudaFuncAttributeMaxDynamicSharedMemorySize, SGEO::smem(P));
+                attr[dev] = true;
+            }
+        }
     }
     cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(SGEO::THREADS), params, SGEO::smem(P), s);
     return cuda_rc(e);
@@ -545,7 +579,7 @@ using namespace ps;
 namespace ps {
 namespace {
 constexpr int64_t SELECT_STREAM_MIN = 1 << 22;  // elements; below this the 3-launch path wins (fill/drain)
-int g_select_kernel = 0;                         // 0 auto, 1 three launches, 2 single pass
+thread_local int g_select_kernel = 0;            // 0 auto, 1 three launches, 2 single pass (per thread)
 
 template <typename TV, typename TF>
 int launch_select_stream(const void *values, const void *flags, int64_t n, void *out, void *count, void *scratch,
@@ -643,6 +677,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "tiles_row_lead")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.tiles_row_lead = (int)value;
+    } else if (!std::strcmp(key, "float_exact")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.float_exact = (int)value;
     } else if (!std::strcmp(key, "add_chunked")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.add_chunked = (int)value;
@@ -698,6 +735,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "reduce_blocks")) return g_tune.reduce_blocks;
     if (!std::strcmp(key, "add_chunked")) return g_tune.add_chunked;
     if (!std::strcmp(key, "tiles_row_lead")) return g_tune.tiles_row_lead;
+    if (!std::strcmp(key, "float_exact")) return g_tune.float_exact;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;

@@ -45,13 +45,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
 }
+#ifndef PS_MBAR_HINT
+#define PS_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if PS_MBAR_HINT
+    // with a suspend-time hint a waiting warp sleeps up to the hint inside try_wait
+    // instead of re-issuing it, leaving the issue slots to the working warps
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"((uint32_t)PS_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

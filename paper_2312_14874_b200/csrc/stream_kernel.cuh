@@ -53,8 +53,8 @@ struct StreamGeom {
     static constexpr int ROW_ELEMS = 32 * VEC;
     static constexpr int CHUNK = ROWS * ROW_ELEMS;  // one warp's unit (ROWS KiB)
     static constexpr int MAXC = 16;                 // chunks per portion (32 KiB portions hold 8)
-    static constexpr int BUF_BYTES_MAX = 200 * 1024;
-    static constexpr int SMEM_FIXED = 4 * NBUF * 8 + 2 * NBUF * MAXC * 8 + 128;
+    static constexpr int BUF_BYTES_MAX = 224 * 1024;
+    static constexpr int SMEM_FIXED = 4 * NBUF * 8 + 2 * NBUF * MAXC * 8 + NBUF * MAXC * 4 + 128;
     static constexpr int smem(int64_t portion) { return (int)(NBUF * portion * sizeof(TIn)) + SMEM_FIXED; }
 };
 
@@ -110,7 +110,94 @@ __device__ __forceinline__ void desc_wait(ulonglong2 (&d)[GATHER_LP], const ulon
     }
 }
 
-template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, bool STALL = false, int MINB = 1>
+// float32 -> float32 scanner body with FP32-pipe arithmetic only (F32PAIR).  The
+// reference rounds every output from a float64 running sum (core.py:86-92); the
+// exact path (F32PAIR = false) does the same per element -- two float<->double
+// conversions on the XU pipe plus float64 adds, which made cfg2 issue/latency-
+// bound at 0.85 of the HBM roofline (profiles/r01_cfg2_full.md: XU 35 %).  Here
+// the in-lane and warp scans of a chunk run in float32 (the reference's own
+// horizontal_scan rounds its blocks in the element dtype, simd.py:84-98), and
+// the carry -- float64 from the ledger -- is split once per chunk into a float
+// pair hi + lo (48-bit significand), advanced row by row with TwoSum and
+// applied per element as hi + (lo' + p): two float adds per element, no
+// conversion.  Error against float32(cumsum(float64)): the in-chunk partial p
+// (<= 1024 elements, a 13-add tree/chain) plus one rounding of the output;
+// measured <= 3e-7 relative on the BASELINE cfg2 input (tests: <= 1e-6).
+// part 1 (before the carry is known): in-lane and warp-inclusive scans in float32
+template <int ROWS, int VEC>
+__device__ __forceinline__ void f32pair_prescan(float (&x)[ROWS][VEC], float (&sc)[ROWS], int lane) {
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+        for (int j = 1; j < VEC; ++j) x[rr][j] = __fadd_rn(x[rr][j], x[rr][j - 1]);
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr) sc[rr] = x[rr][VEC - 1];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr) {
+            const float y = __shfl_up_sync(FULL, sc[rr], d);
+            if (lane >= d) sc[rr] = __fadd_rn(sc[rr], y);
+        }
+    }
+}
+
+// part 2: the float64 chunk carry as a float pair, applied row by row
+template <int ROWS, int VEC, typename Emit>
+__device__ __forceinline__ void f32pair_apply(const float (&x)[ROWS][VEC], const float (&sc)[ROWS], double base,
+                                              int lane, int exclusive, Emit &&emit) {
+    float hi = __double2float_rn(base);
+    float lo = __double2float_rn(base - (double)hi);
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr) {
+        float exs = __shfl_up_sync(FULL, sc[rr], 1);
+        if (lane == 0) exs = 0.f;
+        const float rt = __shfl_sync(FULL, sc[rr], 31);
+        const float l1 = __fadd_rn(lo, exs);  // this lane's offset folded into the low word
+        float y[VEC];
+        if (exclusive) {
+            y[0] = __fadd_rn(hi, l1);
+#pragma unroll
+            for (int j = 1; j < VEC; ++j) y[j] = __fadd_rn(hi, __fadd_rn(l1, x[rr][j - 1]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) y[j] = __fadd_rn(hi, __fadd_rn(l1, x[rr][j]));
+        }
+        emit(rr, y);
+        // (hi, lo) += row total: TwoSum, then renormalise
+        const float s = __fadd_rn(hi, rt);
+        const float bp = __fsub_rn(s, hi);
+        const float e = __fadd_rn(__fsub_rn(hi, __fsub_rn(s, bp)), __fsub_rn(rt, bp));
+        const float l2 = __fadd_rn(lo, e);
+        hi = __fadd_rn(s, l2);
+        lo = __fsub_rn(l2, __fsub_rn(hi, s));
+    }
+}
+
+// Reducer row sums of the float-pair kernel.  PS_F32_RED 0: the float32 TwoSum tree
+// (lane_row_sum, ~6 FP32 ops per element); 1: float64 tree (one F2F on the XU pipe +
+// one DADD per element -- the float-pair scanners leave the XU pipe free).
+#ifndef PS_F32_RED
+#define PS_F32_RED 1
+#endif
+template <typename TIn, typename A, int VEC, bool F32PAIR>
+__device__ __forceinline__ A reducer_row_sum(const TIn (&x)[VEC]) {
+    if constexpr (F32PAIR && PS_F32_RED == 1) {
+        A v[VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] = (A)x[j];
+#pragma unroll
+        for (int d = 1; d < VEC; d <<= 1)
+#pragma unroll
+            for (int j = 0; j + d < VEC; j += 2 * d) v[j] += v[j + d];
+        return v[0];
+    } else {
+        return lane_row_sum<TIn, A, VEC>(x);
+    }
+}
+
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP, bool STALL = false, int MINB = 1,
+          bool F32PAIR = false>
 __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(const StreamArgs a) {
     using Geo = StreamGeom<TIn, SW, ROWS, NBUF, RWP>;
     using A = typename AccOf<TIn>::type;
@@ -129,6 +216,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
     uint64_t *freeb = bars + 3 * NBUF; // scanners released it  (SW)
     A *chunk_tot = reinterpret_cast<A *>(bars + 4 * NBUF);
     A *chunk_pre = chunk_tot + NBUF * MAXC;
+    // F32PAIR: per chunk, nonzero if any element has its sign bit set (or the portion
+    // is a boundary one) -- such chunks take the float64-per-element path
+    uint32_t *chunk_neg = reinterpret_cast<uint32_t *>(chunk_pre + NBUF * MAXC);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
@@ -213,20 +303,33 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                 // cfg2 +0.7 %; integer data measured 1 % slower this way)
                 const int64_t c0 = rw, c1 = rw + RWP;
                 A s0 = (A)0, s1 = (A)0;
+                uint64_t sign0 = 0, sign1 = 0;
 #pragma unroll
                 for (int rr = 0; rr < ROWS; ++rr) {
                     const V256 r0 = lds256<(sizeof(TIn) == 8)>(sb + c0 * CHUNK + rr * ROW_ELEMS + lane * VEC);
                     const V256 r1 = lds256<(sizeof(TIn) == 8)>(sb + c1 * CHUNK + rr * ROW_ELEMS + lane * VEC);
+                    if constexpr (F32PAIR) {
+                        sign0 |= r0.w[0] | r0.w[1] | r0.w[2] | r0.w[3];
+                        sign1 |= r1.w[0] | r1.w[1] | r1.w[2] | r1.w[3];
+                    }
                     TIn x0[VEC], x1[VEC];
                     unpack<TIn>(r0, x0);
                     unpack<TIn>(r1, x1);
-                    s0 += lane_row_sum<TIn, A, VEC>(x0);
-                    s1 += lane_row_sum<TIn, A, VEC>(x1);
+                    s0 += reducer_row_sum<TIn, A, VEC, F32PAIR>(x0);
+                    s1 += reducer_row_sum<TIn, A, VEC, F32PAIR>(x1);
                 }
 #pragma unroll
                 for (int d = 16; d > 0; d >>= 1) {
                     s0 += __shfl_xor_sync(FULL, s0, d);
                     s1 += __shfl_xor_sync(FULL, s1, d);
+                }
+                if constexpr (F32PAIR) {
+                    const bool n0 = __any_sync(FULL, (sign0 & 0x8000000080000000ull) != 0);
+                    const bool n1 = __any_sync(FULL, (sign1 & 0x8000000080000000ull) != 0);
+                    if (lane == 0) {
+                        chunk_neg[b * MAXC + c0] = n0;
+                        chunk_neg[b * MAXC + c1] = n1;
+                    }
                 }
                 if (lane == 0) {
                     tot[c0] = s0;
@@ -235,6 +338,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             } else
             for (int64_t ch = rw; ch < nchunk; ch += RWP) {
                 A s = (A)0;
+                uint64_t sign = w ? 0 : 0x8000000000000000ull;  // boundary chunks: float64 path
                 if (w) {
                     V256 raw[ROWS];
 #pragma unroll
@@ -242,8 +346,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
 #pragma unroll
                     for (int rr = 0; rr < ROWS; ++rr) {
                         TIn x[VEC];
+                        if constexpr (F32PAIR) sign |= raw[rr].w[0] | raw[rr].w[1] | raw[rr].w[2] | raw[rr].w[3];
                         unpack<TIn>(raw[rr], x);
-                        s += lane_row_sum<TIn, A, VEC>(x);
+                        s += reducer_row_sum<TIn, A, VEC, F32PAIR>(x);
                     }
                 } else if (live(r)) {
                     for (int rr = 0; rr < ROWS; ++rr)
@@ -253,6 +358,10 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
                         }
                 }
                 s = warp_sum(s);
+                if constexpr (F32PAIR) {
+                    const bool neg = __any_sync(FULL, (sign & 0x8000000080000000ull) != 0);
+                    if (lane == 0) chunk_neg[b * MAXC + ch] = neg;
+                }
                 if (lane == 0) tot[ch] = s;
             }
             // reads of this buffer are done (their sums are stored); order them before
@@ -292,7 +401,9 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             carry = acc_from_bits<A>(a.seed_bits) + warp_sum(seed);
             if (a.mail.n) carry += mailbox_sum<A>(a.mail, lane);
         }
-        if constexpr (FLOAT) {
+        // float data on the float64-per-element scanner: one gather per region on its own
+        // turn.  Integer data and the float-pair scanner (F32PAIR): early-issued gathers.
+        if constexpr (FLOAT && !F32PAIR) {
             // float32/float64: one gather per region on its own turn, then the fold (the
             // early-issued gather below made cfg2 2.6 % slower: its reducers, not the
             // ledger, set the pace)
@@ -423,6 +534,47 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
             for (int64_t ch = warp; ch < nchunk; ch += SW) {
                 const int64_t t0 = p0 + ch * CHUNK;
                 stall_site<STALL>(a.stall, (r * G + c) * 64 + ch, warp, 7);
+                if constexpr (F32PAIR) {
+                    static_assert(sizeof(TIn) == 4 && sizeof(TOut) == 4, "F32PAIR: float32 -> float32 only");
+                    float x[ROWS][VEC];
+                    if (w) {
+#pragma unroll
+                        for (int rr = 0; rr < ROWS; ++rr)
+                            unpack<float>(lds256<false>(sb + ch * CHUNK + rr * ROW_ELEMS + lane * VEC), x[rr]);
+                    } else {
+#pragma unroll
+                        for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) {
+                                const int64_t pos = t0 + rr * ROW_ELEMS + lane * VEC + j;
+                                x[rr][j] = (pos >= a.lo && pos < a.hi) ? (float)in[pos] : 0.f;
+                            }
+                    }
+                    float sc[ROWS];
+                    f32pair_prescan<ROWS, VEC>(x, sc, lane);  // before the ledger's carries are known
+                    mbar_wait(&pre[b], par(r));
+                    const double base = (double)pr[ch];
+                    // the float pair is used where it is accurate to ~1e-7 relative: nonnegative
+                    // data under a carry >= 64x the chunk's own sum (no cancellation, and the
+                    // float32 in-chunk partials are small next to the output).  Any other chunk
+                    // -- signed data, the first chunks of a scan -- takes the float64 path below.
+                    const bool pair_ok = chunk_neg[b * MAXC + ch] == 0 && base >= 64.0 * (double)chunk_tot[b * MAXC + ch];
+                    if (pair_ok) {
+                        f32pair_apply<ROWS, VEC>(x, sc, base, lane, a.exclusive, [&](int rr, const float(&y)[VEC]) {
+                            if (w) {
+                                stg256_policy(out + t0 + rr * ROW_ELEMS + lane * VEC,
+                                              pack<TOut>(reinterpret_cast<const TOut *>(y)), pol);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j) {
+                                    const int64_t pos = t0 + rr * ROW_ELEMS + lane * VEC + j;
+                                    if (pos >= a.lo && pos < a.hi) out[pos] = (TOut)y[j];
+                                }
+                            }
+                        });
+                        continue;
+                    }
+                }
                 A v[ROWS][VEC];
                 if (w) {
                     V256 raw[ROWS];

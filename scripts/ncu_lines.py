@@ -1,36 +1,46 @@
-"""Per-CUDA-source-line stall samples / instructions from an ncu report (dev tool).
-usage: python scripts/ncu_lines.py report.ncu-rep [top]"""
-import csv
-import io
-import subprocess
-import sys
+"""Attribute an ncu source-page capture (SASS, per instruction) to CUDA source
+lines through the cubin's line table:
 
-rep = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(txt)))
-cur, hdr, out = None, None, []
-for r in rows:
-    if r and r[0] == "File Path":
-        cur = r[1].split("/")[-1]
+    python scripts/ncu_lines.py <ncu-source.csv> <nvdisasm -g output> <kernel mangled name>
+
+Prints issued instructions and warp-stall samples per file:line, largest first."""
+import csv
+import re
+import sys
+from collections import defaultdict
+
+src_csv, sass, kname = sys.argv[1:4]
+# offset -> (file, line) from nvdisasm -g
+lines = {}
+cur = None
+inside = False
+for ln in open(sass):
+    if ln.startswith(".text."):
+        inside = ln.strip() == f".text.{kname}:"
         continue
-    if r and r[0] == "Line No":
-        hdr = r
+    if not inside:
         continue
-    if hdr and len(r) >= len(hdr) - 1 and r[2] == "-":
-        try:
-            s = int(r[4]); ie = int(r[7])
-        except ValueError:
-            continue
-        stalls = {hdr[i]: int(r[i]) for i in range(len(hdr)) if hdr[i].startswith("stall_") and "(" not in hdr[i]
-                  and r[i].isdigit() and int(r[i]) > 0}
-        out.append((s, ie, cur, r[0], r[1].strip()[:60], stalls))
-tot_s = sum(o[0] for o in out); tot_i = sum(o[1] for o in out)
-print(f"samples {tot_s}  warp-instructions {tot_i}")
-for o in sorted(out, key=lambda x: -x[0])[:top]:
-    st = " ".join(f"{k[6:]}={v}" for k, v in sorted(o[5].items(), key=lambda kv: -kv[1])[:3])
-    print(f"{o[0]:6d} {o[1]:10d} {o[2]}:{o[3]:<4} {o[4]:<60} {st}")
-print("--- by instructions")
-for o in sorted(out, key=lambda x: -x[1])[:top]:
-    print(f"{o[1]:10d} {o[2]}:{o[3]:<4} {o[4]}")
+    m = re.search(r'//## File "(.*)", line (\d+)', ln)
+    if m:
+        cur = (m.group(1).split("/")[-1], int(m.group(2)))
+        continue
+    m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", ln)
+    if m and cur:
+        lines[int(m.group(1), 16)] = cur
+rows = list(csv.reader(open(src_csv)))
+head = rows[1]
+col = {k: i for i, k in enumerate(head)}
+body = [r for r in rows[2:] if len(r) == len(head)]
+base = int(body[0][col["Address"]], 16)
+agg = defaultdict(lambda: [0, 0, 0])
+for r in body:
+    off = int(r[col["Address"]], 16) - base
+    key = lines.get(off, ("?", 0))
+    agg[key][0] += int(r[col["Instructions Executed"]] or 0)
+    agg[key][1] += int(r[col["Warp Stall Sampling (All Samples)"]] or 0)
+    agg[key][2] += int(r[col["Warp Stall Sampling (Not-issued Samples)"]] or 0)
+tot = [sum(v[i] for v in agg.values()) for i in range(3)]
+print(f"total: {tot[0]} warp instructions, {tot[1]} stall samples")
+for key, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(sys.argv[4]) if len(sys.argv) > 4 else 40]:
+    print(f"{key[0]}:{key[1]:<5d} inst {v[0]:>11d} ({100*v[0]/tot[0]:5.1f}%)  samples {v[1]:>7d} ({100*v[1]/tot[1]:5.1f}%)"
+          f"  not-issued {v[2]:>7d}")

@@ -241,8 +241,12 @@ def test_every_algorithm_checksum_matches_oracle(device):
 def test_gpu_labels_large_device_resident(algo, elem):
     # above the 32 MiB threshold of the large-input kernels
     rec = run_case(CaseConfig(algo=algo, elem_type=elem, n=(1 << 23) + 5, reps=5, seed=2,
-                              device="cuda", out_of_place=True))
-    assert rec.checksum == checksum(oracle_scan(make_input(elem, (1 << 23) + 5, 2)))
+                              device="cuda", out_of_place=True))  # raises unless within FLOAT_RTOL
+    if elem == "i32":
+        assert rec.checksum == checksum(oracle_scan(make_input(elem, (1 << 23) + 5, 2)))
+    # float32: the stream kernel's float-pair path reassociates (<= 1e-6 relative), so the
+    # CRC of the result need not equal the sequential oracle's -- as for the reference's
+    # own multithreaded float algorithms; run_case has verified the values
     assert rec.bandwidth_gbs > 0
 
 
