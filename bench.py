@@ -578,13 +578,15 @@ def run_ours(args, cfg, cfg_name):
         parity.pop("last_rank_last_output", None)
 
     # ---- timed region: K back-to-back steps between two events on the launching stream ----
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    # (the clock sampler thread starts before the warm-up, so its start-up never delays
+    # the first timed launches; it keeps sampling through the timed region)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t_start.record(stream)
         for _ in range(args.steps):
             step()

@@ -1,0 +1,15 @@
+#!/bin/bash
+# r02 profiles: per config a plain bench run, then the ncu launch list of the same
+# command; full captures of the dominant kernel for cfg5 (headline) and cfg2
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+for c in cfg5 cfg2 cfg1 cfg3 cfg4; do
+  CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu"
+  $CMD > gpurun_out/p_${c}_plain.json 2> gpurun_out/p_${c}_plain.err &&
+  ncu --metrics $M --clock-control none --csv --log-file gpurun_out/p_${c}_launches.csv $CMD > /dev/null 2>&1
+  echo "$c launches rc=$?"
+done
+for c in cfg5 cfg2; do
+  CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu"
+  ncu --set full --clock-control none --import-source on -k regex:scan_ -s 4 -c 1 -o gpurun_out/p_${c}_full $CMD > gpurun_out/p_${c}_full.log 2>&1
+  echo "$c full rc=$?"
+done
