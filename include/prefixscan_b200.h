@@ -71,7 +71,7 @@ extern "C" {
 
 #define PS_OK 0
 #define PS_ERR_DTYPE 1     /* unsupported (dtype_in, dtype_out) pair              */
-#define PS_ERR_ARG 2       /* negative size, NULL buffer, bad leading dimension    */
+#define PS_ERR_ARG 2       /* negative size, NULL or element-misaligned buffer, bad leading dimension */
 #define PS_ERR_SCRATCH 3   /* scratch missing or smaller than ps_*_scratch_bytes   */
 #define PS_ERR_EPOCH 4     /* epoch outside [1, PS_EPOCH_MAX]                      */
 #define PS_ERR_OVERLAP 5   /* in/out partially overlap                             */

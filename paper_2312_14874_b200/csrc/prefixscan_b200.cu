@@ -8,6 +8,8 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <vector>
+#include <cstdio>
 #include <type_traits>
 
 #include "../../include/prefixscan_b200.h"
@@ -16,6 +18,7 @@
 #include "aux_kernels.cuh"
 #include "rounds_kernel.cuh"
 #include "stream_kernel.cuh"
+#include "seg_stream.cuh"
 #include "rows_kernel.cuh"
 #include "select_kernels.cuh"
 #include "select_stream.cuh"
@@ -91,6 +94,7 @@ struct Tuning {
     int add_chunked = 1;                    // ps_add_offset: one CTA per 64 KiB (0 = grid-stride shares)
     int rows_multi = 1;                     // rows kernel: several short rows per buffer (0 = one row per buffer)
     int tiles_row_lead = 1;                 // look-back tiles, batched: 32-byte tile grid per row (0 = shared lead)
+    int seg_kernel = 0;                     // CSR segments: 0 auto, 1 look-back tiles, 2 shared-memory regions
     int float_exact = 0;                    // stream kernel float32 -> float32: 1 = float64 per element (bit-exact
                                             // to float32(cumsum(float64)) whenever the float64 sums are exact)
     Stall stall{};                          // stress tests: in-kernel stall injection (max_ns 0 = off)
@@ -321,6 +325,126 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     }
     cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(SGEO::THREADS), params, SGEO::smem(P), s);
     return cuda_rc(e);
+}
+
+// ---- CSR segments on shared-memory regions (seg_stream.cuh) ---------------------------------------
+constexpr int GSW = 8, GROWS = 4, GNBUF = 6, GRWP = 4;
+#define GGEO SegStreamGeom<TIn, GSW, GROWS, GNBUF, GRWP>
+#define GKERN seg_stream_kernel<TIn, TOut, GSW, GROWS, GNBUF, GRWP>
+constexpr int64_t SEG_STREAM_MAX_GRID = STREAM_MAX_GRID;
+
+template <typename TIn, typename TOut>
+int seg_stream_grid() {
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 0;
+    if (!per_sm[dev]) {
+        cudaFuncSetAttribute(GKERN, cudaFuncAttributeMaxDynamicSharedMemorySize, GGEO::SMEM);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, GKERN, GGEO::THREADS, GGEO::SMEM);
+        per_sm[dev] = b > 0 ? b : -1;
+    }
+    return per_sm[dev] > 0 ? per_sm[dev] * device_sms() : 0;
+}
+
+// scratch of the region kernel: control words, one descriptor per (region, CTA),
+// the portions' lower bounds and repeat flags, then the head bitmap (1 bit per
+// position) -- the last two cleared before and after every call, so the scratch
+// is left as the other entry points expect it (no stray words that could pass
+// for a descriptor)
+struct SegStreamLayout {
+    int64_t Q;  // portions (rounds * G)
+    size_t off_lb, off_dup, off_bm, bm_bytes, total;
+};
+SegStreamLayout seg_stream_layout(int64_t q_portions, int64_t P) {
+    SegStreamLayout L{};
+    L.Q = q_portions;
+    L.off_lb = 256 + align_up((size_t)q_portions * 32, 256);  // integers: two descriptors per portion
+    L.off_dup = L.off_lb + align_up((size_t)(q_portions + 1) * 8, 256);
+    L.off_bm = L.off_dup + align_up((size_t)(q_portions + 1) * 4, 256);
+    L.bm_bytes = align_up((size_t)((q_portions * P + 128 + 7) / 8), 256);
+    L.total = L.off_bm + L.bm_bytes;
+    return L;
+}
+size_t seg_stream_scratch_bytes(int64_t n, int elem_bytes) {
+    const int64_t P = 32768 / elem_bytes;
+    const int64_t q = (n + 32 + P - 1) / P + 2 * SEG_STREAM_MAX_GRID + 1;  // rounds * G <= ceil((lead + n) / P) + G
+    return seg_stream_layout(q, P).total;
+}
+
+// returns -1 when the buffers do not suit the region kernel (caller falls back)
+template <typename TIn, typename TOut>
+int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offsets, int64_t nseg, int exclusive,
+                      void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s) {
+    const uintptr_t ain = (uintptr_t)in % 32;
+    const int64_t lead = (ain % sizeof(TIn)) ? -1 : (int64_t)(ain / sizeof(TIn));
+    const bool vec = lead >= 0 && ((uintptr_t)out % 32) == (uintptr_t)((lead * sizeof(TOut)) % 32) &&
+                     (uintptr_t)out % sizeof(TOut) == 0 && lead * (int64_t)sizeof(TOut) < 32;
+    if (!vec) return -1;
+    const int64_t G = seg_stream_grid<TIn, TOut>();
+    if (G <= 0 || G > SEG_STREAM_MAX_GRID) return -1;
+    const int64_t P = GGEO::P;
+    const int64_t rounds = (lead + n + P * G - 1) / (P * G);
+    const SegStreamLayout L = seg_stream_layout(rounds * G, P);
+    if (!scratch || scratch_bytes < L.total) return PS_ERR_SCRATCH;
+    char *sc = static_cast<char *>(scratch);
+    SegStreamArgs a{};
+    a.in = static_cast<const TIn *>(in) - lead;
+    a.out = static_cast<TOut *>(out) - lead;
+    a.lo = lead;
+    a.hi = lead + n;
+    a.lead = lead;
+    a.portion = P;
+    a.rounds = rounds;
+    a.offsets = offsets;
+    a.nseg = nseg;
+    int64_t *lb = reinterpret_cast<int64_t *>(sc + L.off_lb);
+    uint32_t *dup = reinterpret_cast<uint32_t *>(sc + L.off_dup);
+    uint32_t *bm = reinterpret_cast<uint32_t *>(sc + L.off_bm);
+    a.lb = lb;
+    a.dupflag = dup;
+    a.bitmap = bm;
+    a.totals = totals;
+    a.desc = reinterpret_cast<ulonglong2 *>(sc + 256);
+    a.epoch = epoch;
+    a.exclusive = exclusive;
+    a.inflight = g_tune.stream_inflight;
+    const size_t clear = L.total - L.off_dup;  // repeat flags + bitmap
+    cudaError_t e = cudaMemsetAsync(dup, 0, clear, s);
+    if (e != cudaSuccess) return cuda_rc(e);
+    const int64_t threads = (L.Q + 1 > nseg + 1 ? L.Q + 1 : nseg + 1);
+    seg_prepare_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(offsets, nseg, n, lead, P, L.Q, lb, dup, bm);
+    void *params[] = {&a};
+#ifdef PS_SEG_TRACE
+    static uint64_t *trace = nullptr;
+    const size_t tbytes = (size_t)rounds * G * 8 * 8;
+    static size_t tcap = 0;
+    if (tcap < tbytes) {
+        if (trace) cudaFree(trace);
+        cudaMalloc(&trace, tbytes);
+        tcap = tbytes;
+        cudaMemcpyToSymbol(g_seg_trace, &trace, sizeof(trace));
+    }
+    cudaMemsetAsync(trace, 0, tbytes, s);
+#endif
+    e = cudaLaunchCooperativeKernel((const void *)GKERN, dim3((unsigned)G), dim3(GGEO::THREADS), params, GGEO::SMEM, s);
+    if (e != cudaSuccess) return cuda_rc(e);
+#ifdef PS_SEG_TRACE
+    {
+        std::vector<uint64_t> h(tbytes / 8);
+        cudaMemcpyAsync(h.data(), trace, tbytes, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        FILE *f = std::fopen("gpurun_out/seg_trace.bin", "wb");
+        if (f) {
+            const int64_t hdr[2] = {rounds, G};
+            std::fwrite(hdr, 8, 2, f);
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
+#endif
+    return cuda_rc(cudaMemsetAsync(dup, 0, clear, s));
 }
 
 // ---- batched rows, one CTA per row (rows_kernel.cuh) ----------------------------------------------
@@ -677,6 +801,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "tiles_row_lead")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.tiles_row_lead = (int)value;
+    } else if (!std::strcmp(key, "seg_kernel")) {
+        if (value < 0 || value > 2) return PS_ERR_ARG;
+        g_tune.seg_kernel = (int)value;
     } else if (!std::strcmp(key, "float_exact")) {
         if (value < 0 || value > 1) return PS_ERR_ARG;
         g_tune.float_exact = (int)value;
@@ -736,6 +863,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "add_chunked")) return g_tune.add_chunked;
     if (!std::strcmp(key, "tiles_row_lead")) return g_tune.tiles_row_lead;
     if (!std::strcmp(key, "float_exact")) return g_tune.float_exact;
+    if (!std::strcmp(key, "seg_kernel")) return g_tune.seg_kernel;
     if (!std::strcmp(key, "stall_seed")) return g_tune.stall.seed;
     if (!std::strcmp(key, "stall_prob")) return g_tune.stall.prob;
     if (!std::strcmp(key, "stall_ns")) return g_tune.stall.max_ns;
@@ -800,6 +928,7 @@ int ps_reduce(const void *in, int64_t n, int dtype_in, uint64_t seed_bits, const
               int64_t n_seed_terms, void *total_out, void *scratch, size_t scratch_bytes, void *stream) {
     if (!dsize(dtype_in)) return PS_ERR_DTYPE;
     if (n < 0 || !total_out || (n > 0 && !in)) return PS_ERR_ARG;
+    if ((uintptr_t)in % dsize(dtype_in)) return PS_ERR_ARG;  // element-misaligned: not a typed array
     if (!scratch || scratch_bytes < ps_reduce_scratch_bytes(n, dtype_in)) return PS_ERR_SCRATCH;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int dev = 0, sms = 148;
@@ -813,7 +942,7 @@ int ps_reduce(const void *in, int64_t n, int dtype_in, uint64_t seed_bits, const
     a.in = in;
     a.n = n;
     const uintptr_t ain = (uintptr_t)in % 32;
-    a.lead = (ain % dsize(dtype_in)) ? n : (int64_t)(((32 - ain) % 32) / dsize(dtype_in));
+    a.lead = (int64_t)(((32 - ain) % 32) / dsize(dtype_in));
     a.seed_bits = seed_bits;
     a.seed_terms = seed_terms;
     a.n_seed_terms = n_seed_terms;
@@ -842,13 +971,14 @@ int ps_add_offset(void *buf, int64_t n, int dtype, uint64_t delta_bits, const vo
                   int64_t n_delta_terms, void *stream) {
     if (!dsize(dtype)) return PS_ERR_DTYPE;
     if (n < 0 || (n > 0 && !buf) || n_delta_terms < 0) return PS_ERR_ARG;
+    if ((uintptr_t)buf % dsize(dtype)) return PS_ERR_ARG;  // element-misaligned: not a typed array
     if (n == 0) return PS_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uintptr_t ab = (uintptr_t)buf % 32;
-    const int64_t lead = (ab % dsize(dtype)) ? n : (int64_t)(((32 - ab) % 32) / dsize(dtype));
+    const int64_t lead = (int64_t)(((32 - ab) % 32) / dsize(dtype));
     const int64_t vec = 32 / (int64_t)dsize(dtype);
     int64_t want = (n / vec + 255) / 256;
     int64_t grid = want < (int64_t)sms * 8 ? want : (int64_t)sms * 8;
@@ -870,7 +1000,8 @@ int ps_add_offset(void *buf, int64_t n, int dtype, uint64_t delta_bits, const vo
 
 size_t ps_scan_segmented_scratch_bytes(int64_t n, int dtype_in, int dtype_out) {
     if (!pair_ok(dtype_in, dtype_out) || n < 0) return 0;
-    return seg_scratch_bytes(n, (int)dsize(dtype_in));
+    const size_t a = seg_scratch_bytes(n, (int)dsize(dtype_in)), b = seg_stream_scratch_bytes(n, (int)dsize(dtype_in));
+    return a > b ? a : b;
 }
 
 int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_offsets, int64_t nseg,
@@ -889,8 +1020,19 @@ int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_o
     if (overlaps_partially(in, (size_t)n * dsize(dtype_in), out, (size_t)n * dsize(dtype_out))) return PS_ERR_OVERLAP;
     if (in == out && dsize(dtype_in) != dsize(dtype_out)) return PS_ERR_OVERLAP;
     if (!scratch || scratch_bytes < seg_scratch_bytes(n, (int)dsize(dtype_in))) return PS_ERR_SCRATCH;
-#define CALL(TI, TO) \
-    return launch_segmented<TI, TO>(in, out, n, seg_offsets, nseg, exclusive, seg_totals, scratch, epoch, s)
+    // large inputs: the shared-memory-region kernel (one HBM read + write per element);
+    // small ones, or buffers it cannot stream: the look-back tiles
+    const bool big = n * (int64_t)dsize(dtype_in) >= g_tune.rounds_min_bytes;
+    const bool regions = g_tune.seg_kernel == 2 || (g_tune.seg_kernel == 0 && big);
+#define CALL(TI, TO)                                                                                           \
+    {                                                                                                          \
+        if (regions) {                                                                                         \
+            const int rc = launch_seg_stream<TI, TO>(in, out, n, seg_offsets, nseg, exclusive, seg_totals,      \
+                                                     scratch, scratch_bytes, epoch, s);                        \
+            if (rc >= 0) return rc;                                                                            \
+        }                                                                                                      \
+        return launch_segmented<TI, TO>(in, out, n, seg_offsets, nseg, exclusive, seg_totals, scratch, epoch, s); \
+    }
     PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);
 #undef CALL
 }

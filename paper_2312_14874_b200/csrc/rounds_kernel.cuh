@@ -67,6 +67,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 #endif
 }
+// mbarrier wait that suspends the warp in try_wait (up to `hint_ns` per attempt)
+// instead of re-issuing it: for kernels whose spinning roles would otherwise
+// take the issue slots of the working ones
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t hint_ns = 1000000u) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

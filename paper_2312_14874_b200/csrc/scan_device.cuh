@@ -75,6 +75,12 @@ __device__ __forceinline__ void stg256_stream(void *p, const V256 &v) {
 template <typename A> __device__ __forceinline__ A shfl_up(A v, int d) {
     return __shfl_up_sync(FULL, v, d);
 }
+template <typename A> __device__ __forceinline__ A shfl_xor(A v, int d) {
+    return __shfl_xor_sync(FULL, v, d);
+}
+template <typename A> __device__ __forceinline__ A shfl_down(A v, int d) {
+    return __shfl_down_sync(FULL, v, d);
+}
 template <typename A> __device__ __forceinline__ A shfl_idx(A v, int src) {
     return __shfl_sync(FULL, v, src);
 }

@@ -1,0 +1,844 @@
+// seg_stream.cuh -- CSR-segmented scans on the shared-memory-region
+// accumulate-scan (the stream kernel's structure, stream_kernel.cuh).
+//
+// Segment s is in[off[s] .. off[s+1]); every segment restarts at zero and
+// seg_totals[s] receives its sum (ps_scan_segmented).  The reference has no
+// kernel of this shape: it is the general form of the per-chunk scans of
+// simd.py:164-206 with chunk boundaries from an offsets array.  The look-back
+// form (segmented.cuh) is bound by the carry chain's L2 round trips; here the
+// data streams through shared memory exactly as for a plain 1-D scan -- one
+// HBM read and one write per element -- and the segments only change the
+// operator: the segmented sum on (head flag, value) pairs,
+//     (f1, v1) . (f2, v2) = (f1 | f2,  f2 ? v2 : v1 + v2),
+// applied by every role in a fixed order (deterministic float results).
+//
+// A pre-pass (seg_prepare_kernel) scatters the offsets into a head bitmap in
+// global memory (1 bit per position) and computes, per CTA portion q (P
+// positions of region r, q = r * G + c), the lower bound lb[q] of its start in
+// the offsets and a flag for repeated offsets (empty segments) inside it.  Roles:
+//   producer    TMA bulk copies of the portion and of its slice of the head bitmap
+//               (plus the next 128 bits) into slot r % NBUF
+//   head warp   per slot: counts of heads before every 32-position word (prefix
+//               popcounts, for the segment index of a total) and the portion's
+//               lb / flags (prefetched 32 regions at a time)
+//   reducers    per-chunk segmented aggregates (f, v) from shared memory;
+//               the portion aggregate -> the region's descriptor (flag in bit 62)
+//   ledger      grid-wide gather of the region's G portion aggregates, segmented
+//               fold -> one carry per chunk
+//   scanners    segmented in-lane / warp scans of each chunk, the chunk carry
+//               applied where no head precedes; each element followed by a head
+//               (a segment's last element) writes the segment total
+#pragma once
+#ifndef PS_SEG_EXP
+#define PS_SEG_EXP 0
+#endif
+#ifndef PS_SEG_SLEEP
+#define PS_SEG_SLEEP 1
+#endif
+#if PS_SEG_SLEEP
+#define SEG_WAIT(bar, par) mbar_wait_sleep(bar, par)
+#else
+#define SEG_WAIT(bar, par) mbar_wait(bar, par)
+#endif
+#ifndef PS_SEG_UNROLL
+#define PS_SEG_UNROLL 1
+#endif
+#ifdef PS_SEG_TRACE  // development builds only: per (region, CTA) timestamps of the role hand-offs
+__device__ uint64_t *g_seg_trace;
+#define SEG_TRACE(r, k)                                                                        \
+    do {                                                                                       \
+        if (g_seg_trace) {                                                                     \
+            uint64_t t_;                                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            g_seg_trace[((r) * gridDim.x + blockIdx.x) * 8 + (k)] = t_;                        \
+        }                                                                                      \
+    } while (0)
+#else
+#define SEG_TRACE(r, k) do { } while (0)
+#endif
+
+#include "stream_kernel.cuh"
+
+namespace ps {
+
+constexpr int SEG_UNROLL = PS_SEG_UNROLL;  // scanner rows per loop body (code size vs ILP; measured)
+constexpr uint64_t SEG_FLAG = 1ull << 62;  // descriptor word: the portion holds a segment head
+
+struct SegStreamArgs {
+    const void *in;   // aligned base: position p <-> element p - lead
+    void *out;
+    int64_t lo, hi;   // valid positions
+    int64_t lead;
+    int64_t portion;  // positions per CTA per region
+    int64_t rounds;
+    const int64_t *offsets;  // nseg + 1 entries
+    int64_t nseg;
+    const int64_t *lb;       // [rounds * G + 1]: lower_bound(offsets, q * P - lead) << 2
+    const uint32_t *dupflag; // [rounds * G + 1]: nonzero if offsets repeat inside portion q
+    const uint32_t *bitmap;  // head bitmap by position, rounds * G * P + 128 bits
+    void *totals;            // acc-typed per segment, pre-zeroed; nullable
+    ulonglong2 *desc;        // rounds * G descriptors (+ rounds * G more for integers: head info)
+    uint32_t epoch;
+    int exclusive;
+    int inflight;
+};
+
+// Pre-pass, one thread per portion boundary and per offset:
+//   lb[q] (q <= Q)  = first s in [0, nseg] with off[s] >= q * P - lead (nseg + 1 if none),
+//                     stored << 2 so no word of it can pass for a published descriptor;
+//   bitmap          bit (off[s] + lead) set for every offset (the terminal off[nseg] = n too);
+//   dupflag[q]      4 if two offsets coincide inside portion q (empty segments).
+// bitmap and dupflag must be zero on entry (the launcher clears them before and after).
+__global__ void seg_prepare_kernel(const int64_t *off, int64_t nseg, int64_t n, int64_t lead, int64_t P,
+                                   int64_t Q, int64_t *lb, uint32_t *dupflag, uint32_t *bitmap) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t <= nseg) {
+        const int64_t e = __ldg(off + t);
+        const int64_t pos = e + lead;
+        atomicOr(bitmap + (pos >> 5), 1u << (pos & 31));
+        if (t > 0 && __ldg(off + t - 1) == e) atomicOr(dupflag + pos / P, 4u);
+    }
+    if (t > Q) return;
+    const int64_t e = t * P - lead;
+    int64_t res;
+    if (e <= 0) {
+        res = 0;
+    } else if (e > n) {
+        res = nseg + 1;
+    } else {
+        // galloping from the uniform-segment guess, then bisection on [lo, hi):
+        // off[lo - 1] < e <= off[hi] (virtual off[-1] = -inf)
+        int64_t g = (int64_t)((double)e / (double)n * (double)nseg);
+        if (g > nseg) g = nseg;
+        if (g < 0) g = 0;
+        int64_t lo, hi;
+        if (__ldg(off + g) >= e) {
+            hi = g;
+            int64_t step = 1;
+            while (hi - step >= 0 && __ldg(off + hi - step) >= e) {
+                hi -= step;
+                step <<= 1;
+            }
+            lo = hi - step + 1 > 0 ? hi - step + 1 : 0;
+        } else {
+            lo = g + 1;
+            int64_t step = 1;
+            while (lo + step - 1 <= nseg && __ldg(off + lo + step - 1) < e) {
+                lo += step;
+                step <<= 1;
+            }
+            hi = lo + step - 1 <= nseg ? lo + step - 1 : nseg + 1;
+        }
+        while (lo < hi) {  // first index in [lo, hi) with off >= e; hi if none
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(off + mid) >= e) hi = mid;
+            else lo = mid + 1;
+        }
+        res = lo;
+    }
+    lb[t] = res << 2;
+}
+
+template <typename A> struct SegPair {
+    A v;
+    uint32_t f;
+};
+template <typename A> __device__ __forceinline__ SegPair<A> seg_combine(const SegPair<A> &a, const SegPair<A> &b) {
+    return SegPair<A>{b.f ? b.v : a.v + b.v, a.f | b.f};
+}
+template <typename A> __device__ __forceinline__ SegPair<A> seg_shfl_up(const SegPair<A> &p, int d) {
+    return SegPair<A>{shfl_up(p.v, d), __shfl_up_sync(FULL, p.f, d)};
+}
+// inclusive segmented scan across the warp (lane order)
+template <typename A> __device__ __forceinline__ SegPair<A> seg_warp_scan(SegPair<A> p, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const SegPair<A> y = seg_shfl_up(p, d);
+        if (lane >= d) p = seg_combine(y, p);
+    }
+    return p;
+}
+
+struct SegMeta {       // per buffer slot, written by the head warp
+    int64_t lb0, lb1;  // the portion's offsets: off[lb0 .. lb1)
+    int32_t dup, next_head, live, pad;
+};
+
+template <typename TIn, int SW, int ROWS, int NBUF, int RWP>
+struct SegStreamGeom {
+    static constexpr int WARPS = SW + RWP + 3;  // + producer, ledger, head warp
+    static constexpr int THREADS = WARPS * 32;
+    static constexpr int VEC = 32 / sizeof(TIn);
+    static constexpr int ROW_ELEMS = 32 * VEC;
+    static constexpr int CHUNK = ROWS * ROW_ELEMS;
+    static constexpr int MAXC = 16;
+    static constexpr int64_t P = 32768 / sizeof(TIn);  // 32 KiB of input per CTA per region
+    static constexpr int WORDS = (int)(P / 32);         // head bitmap words per portion
+    static constexpr int BMW = WORDS + 4;               // per slot: + the next 128 positions (TMA: 16 B units)
+    using Meta = SegMeta;
+    static constexpr int SMEM_FIXED = NBUF * BMW * 4 + 5 * NBUF * 8 + 4 * NBUF * MAXC * 8 + NBUF * MAXC * 4 +
+                                      NBUF * WORDS * 4 + NBUF * (int)sizeof(Meta) + 128;
+    static constexpr int SMEM = (int)(NBUF * P * sizeof(TIn)) + SMEM_FIXED;
+};
+
+template <typename TIn, typename TOut, int SW, int ROWS, int NBUF, int RWP>
+__global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(const SegStreamArgs a) {
+    using Geo = SegStreamGeom<TIn, SW, ROWS, NBUF, RWP>;
+    using A = typename AccOf<TIn>::type;
+    using Pair = SegPair<A>;
+    using Meta = typename Geo::Meta;
+    constexpr int VEC = Geo::VEC, ROW_ELEMS = Geo::ROW_ELEMS, CHUNK = Geo::CHUNK, MAXC = Geo::MAXC;
+    constexpr int WORDS = Geo::WORDS, BMW = Geo::BMW;
+    constexpr int64_t P = Geo::P;
+    constexpr int64_t NCHUNK = P / CHUNK;
+    constexpr uint32_t VMASK = (VEC == 32) ? 0xffffffffu : ((1u << VEC) - 1);
+    constexpr int RT = RWP * 32;
+    constexpr int BAR_RED = 1;
+    constexpr int W_PROD = SW + RWP, W_LEDGER = SW + RWP + 1, W_HEAD = SW + RWP + 2;
+    static_assert(NCHUNK <= MAXC && NCHUNK <= 32, "chunks per portion");
+    // integers: "subtract the segment base" form -- out = S - B with S the plain running
+    // sum and B = S before the last head at or before the element (exact in two's
+    // complement); floats: the (flag, value) pair operator (no cancellation)
+    constexpr bool SUB = (A)0.5 == (A)0;
+    static_assert(32 % VEC == 0, "a lane's head bits sit in one bitmap word");
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TIn *buf = reinterpret_cast<TIn *>(smem_raw);
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem_raw + (size_t)NBUF * P * sizeof(TIn));  // TMA'd
+    uint64_t *bars = reinterpret_cast<uint64_t *>(bitmap + NBUF * BMW);
+    uint64_t *full = bars;              // TMA landed            (1 arrival + tx)
+    uint64_t *hdr = bars + NBUF;        // head counts and meta  (1)
+    uint64_t *red = bars + 2 * NBUF;    // chunk aggregates      (1)
+    uint64_t *pre = bars + 3 * NBUF;    // chunk carries         (1)
+    uint64_t *freeb = bars + 4 * NBUF;  // scanners released it  (SW)
+    A *chunk_tot = reinterpret_cast<A *>(bars + 5 * NBUF);
+    A *chunk_pre = chunk_tot + NBUF * MAXC;
+    A *chunk_plh = chunk_pre + NBUF * MAXC;  // SUB: chunk sum before its last head (reducers)
+    A *chunk_B = chunk_plh + NBUF * MAXC;    // SUB: S before the last head preceding the chunk (ledger)
+    uint32_t *chunk_f = reinterpret_cast<uint32_t *>(chunk_B + NBUF * MAXC);
+    int32_t *cntb = reinterpret_cast<int32_t *>(chunk_f + NBUF * MAXC);
+    Meta *meta = reinterpret_cast<Meta *>(cntb + NBUF * WORDS);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const TIn *in = reinterpret_cast<const TIn *>(a.in);
+    TOut *out = reinterpret_cast<TOut *>(a.out);
+    const uint64_t want = (uint64_t)a.epoch << 2;
+
+    if (tid == 0) {
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&hdr[b], 1);
+            mbar_init(&red[b], 1);
+            mbar_init(&pre[b], 1);
+            mbar_init(&freeb[b], SW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto par = [&](int64_t r) { return (uint32_t)((r / NBUF) & 1); };
+    auto p0_of = [&](int64_t r) { return (r * G + c) * P; };
+    auto whole = [&](int64_t r) {
+        const int64_t p0 = p0_of(r);
+        return p0 >= a.lo && p0 + P <= a.hi;
+    };
+    auto live = [&](int64_t r) {
+        const int64_t p0 = p0_of(r);
+        return p0 + P > a.lo && p0 < a.hi;
+    };
+    // head bits of the VEC positions at portion-relative position q0 (a multiple of VEC)
+    auto heads_at = [&](const uint32_t *bm, int64_t q0) {
+        return (bm[q0 >> 5] >> (q0 & 31)) & VMASK;
+    };
+
+    if (warp == W_PROD) {
+        // ============================ producer ===================================
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                if (r >= NBUF) SEG_WAIT(&freeb[b], par(r - NBUF));
+                if (r >= a.inflight && a.inflight > 0 && a.inflight < NBUF)
+                    SEG_WAIT(&full[(r - a.inflight) % NBUF], par(r - a.inflight));
+                // the portion's slice of the head bitmap (+ the next 128 positions) always;
+                // its data when the portion is whole (boundary portions read global memory)
+                constexpr uint32_t BM_BYTES = (uint32_t)BMW * 4;
+                const bool w = whole(r);
+                const uint32_t bytes = w ? (uint32_t)(P * sizeof(TIn)) : 0u;
+                mbar_expect_tx(&full[b], bytes + BM_BYTES);
+                bulk_g2s(bitmap + b * BMW, a.bitmap + (p0_of(r) >> 5), BM_BYTES, &full[b], pol);
+                SEG_TRACE(r, 0);
+                if (w) {
+                    constexpr uint32_t PIECE = 16384;
+                    const char *src = reinterpret_cast<const char *>(in + p0_of(r));
+                    char *dst = reinterpret_cast<char *>(buf + (size_t)b * P);
+                    for (uint32_t o = 0; o < bytes; o += PIECE)
+                        bulk_g2s(dst + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, &full[b], pol);
+                }
+            }
+        }
+        return;
+    }
+
+    if (warp == W_HEAD) {
+        // ============================ head warp ==================================
+        constexpr int PER = WORDS / 32;
+        int64_t pf_lb0 = 0, pf_lb1 = 0;  // lane k: portion (r0 + k) of this CTA, prefetched
+        uint32_t pf_dup = 0;
+        for (int64_t r = 0; r < a.rounds; ++r) {
+            const int b = (int)(r % NBUF);
+            if ((r & 31) == 0) {  // one round trip per 32 regions
+                const int64_t rk = r + lane;
+                if (rk < a.rounds) {
+                    const int64_t q = rk * G + c;
+                    pf_lb0 = a.lb[q] >> 2;
+                    pf_lb1 = a.lb[q + 1] >> 2;
+                    pf_dup = a.dupflag[q];
+                }
+            }
+            const int k = (int)(r & 31);
+            const int64_t s0 = __shfl_sync(FULL, pf_lb0, k), s1 = __shfl_sync(FULL, pf_lb1, k);
+            const uint32_t dup = __shfl_sync(FULL, pf_dup, k);
+            if (r >= NBUF) SEG_WAIT(&freeb[b], par(r - NBUF));
+            SEG_WAIT(&full[b], par(r));  // the bitmap slice has landed
+            const uint32_t *bm = bitmap + b * BMW;
+            int32_t *cb = cntb + b * WORDS;
+            // heads before each 32-position word: exclusive scan of popcounts
+            int32_t v[PER], run = 0;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                v[j] = run;
+                run += __popc(bm[lane * PER + j]);
+            }
+            int32_t incl = run;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int32_t y = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int32_t ex = incl - run;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) cb[lane * PER + j] = ex + v[j];
+            if (lane == 0) {
+                Meta m;
+                m.lb0 = s0;
+                m.lb1 = s1;
+                m.dup = dup != 0;
+                m.next_head = (int32_t)(bm[WORDS] & 1u);
+                m.live = live(r);
+                m.pad = 0;
+                meta[b] = m;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr[b]);
+        }
+        return;
+    }
+
+    if (warp >= SW && warp < W_PROD) {
+        // ============================ reducers ===================================
+        const int rw = warp - SW;
+        if constexpr (SUB) {
+            // per chunk: plain sum, and the sum of the elements before its last head
+            ulonglong2 *desc2 = a.desc + a.rounds * G;
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                SEG_WAIT(&full[b], par(r));
+                if (rw == 0 && lane == 0) SEG_TRACE(r, 1);
+                const TIn *sb = buf + (size_t)b * P;
+                const uint32_t *bm = bitmap + b * BMW;
+                const int64_t p0 = p0_of(r);
+                const bool w = whole(r);
+                const bool lv = w || live(r);
+                for (int64_t ch = rw; ch < NCHUNK; ch += RWP) {
+                    A s = (A)0, pl = (A)0;
+                    int lastpos = -1;
+                    if (lv) {
+                        TIn x[ROWS][VEC];
+#pragma unroll
+                        for (int rr = 0; rr < ROWS; ++rr) {
+                            const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
+                            if (w) {
+                                unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x[rr]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j) {
+                                    const int64_t pos = p0 + q0 + j;
+                                    x[rr][j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
+                                }
+                            }
+                            const uint32_t hb = heads_at(bm, q0);
+#if PS_SEG_EXP == 2 || PS_SEG_EXP == 4
+                            (void)hb;
+#else
+                            if (hb) lastpos = rr * ROW_ELEMS + lane * VEC + (31 - __clz((int)hb));
+#endif
+                        }
+                        const int lh = __reduce_max_sync(FULL, lastpos);  // the chunk's last head (-1: none)
+#pragma unroll
+                        for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) {
+                                const A v = (A)x[rr][j];
+                                s += v;
+                                if (rr * ROW_ELEMS + lane * VEC + j < lh) pl += v;
+                            }
+                        lastpos = lh;
+                    }
+                    s = warp_sum(s);
+                    pl = warp_sum(pl);
+                    if (lane == 0) {
+                        chunk_tot[b * MAXC + ch] = s;
+                        chunk_plh[b * MAXC + ch] = pl;
+                        chunk_f[b * MAXC + ch] = lastpos >= 0;
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                named_sync(BAR_RED, RT);
+                if (rw == 0) {
+                    // the portion (lanes = chunks): total, and the sum before its last head
+                    const A ct = lane < NCHUNK ? chunk_tot[b * MAXC + lane] : (A)0;
+                    const uint32_t fb = __ballot_sync(FULL, lane < NCHUNK && chunk_f[b * MAXC + lane] != 0u);
+                    const int kl = fb ? 31 - __clz((int)fb) : -1;
+                    const A t = warp_sum(ct);
+                    const A before = warp_sum(lane < kl ? ct : (A)0);
+                    const A plh = before + (kl >= 0 ? chunk_plh[b * MAXC + kl] : (A)0);
+                    if (lane == 0) {
+                        st_desc(desc2 + r * G + c, want | ST_A | (fb ? SEG_FLAG : 0ull), acc_to_bits<A>(plh));
+                        st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
+                        SEG_TRACE(r, 2);
+                        mbar_arrive(&red[b]);
+                    }
+                }
+                named_sync(BAR_RED, RT);
+            }
+            return;
+        }
+        for (int64_t r = 0; r < a.rounds; ++r) {
+            const int b = (int)(r % NBUF);
+            SEG_WAIT(&full[b], par(r));  // data and head bits (the reducers need no counts)
+            if (rw == 0 && lane == 0) SEG_TRACE(r, 1);
+            const TIn *sb = buf + (size_t)b * P;
+            const uint32_t *bm = bitmap + b * BMW;
+            const int64_t p0 = p0_of(r);
+            const bool w = whole(r);
+            const bool lv = w || live(r);
+            for (int64_t ch = rw; ch < NCHUNK; ch += RWP) {
+                Pair agg{(A)0, 0u};
+                if (lv) {
+#pragma unroll
+                    for (int rr = 0; rr < ROWS; ++rr) {
+                        const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
+                        TIn x[VEC];
+                        if (w) {
+                            unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) {
+                                const int64_t pos = p0 + q0 + j;
+                                x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
+                            }
+                        }
+                        const uint32_t hb = heads_at(bm, q0);
+                        Pair lp{(A)0, hb != 0u};
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) lp.v = ((hb >> j) & 1u) ? (A)x[j] : lp.v + (A)x[j];
+                        // ordered reduction over the lanes of the row: lane 0 ends with it
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const Pair y{shfl_down(lp.v, d), __shfl_down_sync(FULL, lp.f, d)};
+                            if ((lane & (2 * d - 1)) == 0) lp = seg_combine(lp, y);
+                        }
+                        agg = seg_combine(agg, lp);  // meaningful on lane 0
+                    }
+                }
+                if (lane == 0) {
+                    chunk_tot[b * MAXC + ch] = agg.v;
+                    chunk_f[b * MAXC + ch] = agg.f;
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            named_sync(BAR_RED, RT);
+            if (rw == 0 && lane == 0) {
+                Pair t{(A)0, 0u};
+                for (int64_t ch = 0; ch < NCHUNK; ++ch) t = seg_combine(t, Pair{chunk_tot[b * MAXC + ch], chunk_f[b * MAXC + ch]});
+                st_desc(a.desc + r * G + c, want | ST_A | (t.f ? SEG_FLAG : 0ull), acc_to_bits<A>(t.v));
+                SEG_TRACE(r, 2);
+                mbar_arrive(&red[b]);
+            }
+            named_sync(BAR_RED, RT);
+        }
+        return;
+    }
+
+    if (warp == W_LEDGER) {
+        // ============================ ledger =====================================
+        if constexpr (SUB) {
+            // plain carries as the 1-D stream kernel, plus the running sum before the last
+            // head seen so far (B), region by region
+            ulonglong2 *desc2 = a.desc + a.rounds * G;
+            A carry = (A)0, bcarry = (A)0;
+            ulonglong2 dn[GATHER_LP], dh[GATHER_LP];
+            desc_issue(dn, a.desc, G, lane);
+            desc_issue(dh, desc2, G, lane);
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                SEG_WAIT(&red[b], par(r));
+                if (lane == 0) SEG_TRACE(r, 3);
+                // chunks of this portion: exclusive prefix of the sums, and per chunk the
+                // portion-relative S before the last head of an earlier chunk
+                const A ct = lane < NCHUNK ? chunk_tot[b * MAXC + lane] : (A)0;
+                const uint32_t cf = lane < NCHUNK ? chunk_f[b * MAXC + lane] : 0u;
+                const A cpl = lane < NCHUNK ? chunk_plh[b * MAXC + lane] : (A)0;
+                A cinc = ct;
+#pragma unroll
+                for (int d = 1; d < NCHUNK; d <<= 1) {  // lanes >= NCHUNK hold nothing anyone reads
+                    const A y = shfl_up(cinc, d);
+                    if (lane >= d) cinc += y;
+                }
+                const A cex = cinc - ct;
+                const uint32_t cfb = __ballot_sync(FULL, cf != 0u);
+                const uint32_t cbelow = cfb & ((1u << lane) - 1u);
+                const A chead = shfl_idx(cex + cpl, cbelow ? 31 - __clz((int)cbelow) : 0);
+                // the region's G portion totals and head infos
+                {
+                    unsigned pending = 0;
+#pragma unroll
+                    for (int i = 0; i < GATHER_LP; ++i)
+                        if (lane + 32 * i < G) pending |= 1u << i;
+                    while (true) {
+#pragma unroll
+                        for (int i = 0; i < GATHER_LP; ++i)
+                            if (((pending >> i) & 1) && (dn[i].x & ~3ull) == want && (dn[i].x & 3ull) != 0 &&
+                                (dh[i].x & ~(3ull | SEG_FLAG)) == want && (dh[i].x & 3ull) != 0)
+                                pending &= ~(1u << i);
+                        if (!__any_sync(FULL, pending != 0)) break;
+                        __nanosleep(32);
+#pragma unroll
+                        for (int i = 0; i < GATHER_LP; ++i)
+                            if ((pending >> i) & 1) {
+                                dn[i] = ld_desc(a.desc + r * G + lane + 32 * i);
+                                dh[i] = ld_desc(desc2 + r * G + lane + 32 * i);
+                            }
+                    }
+                }
+                if (lane == 0) SEG_TRACE(r, 4);
+                A tv[GATHER_LP], hv[GATHER_LP];
+                uint32_t hf[GATHER_LP];
+#pragma unroll
+                for (int i = 0; i < GATHER_LP; ++i) {
+                    const bool ok = lane + 32 * i < G;
+                    tv[i] = ok ? acc_from_bits<A>(dn[i].y) : (A)0;
+                    hv[i] = ok ? acc_from_bits<A>(dh[i].y) : (A)0;
+                    hf[i] = ok && (dh[i].x & SEG_FLAG) ? 1u : 0u;
+                }
+                if (r + 1 < a.rounds) {
+                    desc_issue(dn, a.desc + (r + 1) * G, G, lane);
+                    desc_issue(dh, desc2 + (r + 1) * G, G, lane);
+                }
+                // no scan over the G portions is needed, only masked sums: S at this CTA's
+                // portion (sum of the totals before c), at the last head-holding portion before
+                // c (j1) and at the last one of the region (j2), and the region total
+                int j1 = -1, j2 = -1;
+#pragma unroll
+                for (int i = 0; i < GATHER_LP; ++i) {
+                    const uint32_t fb = __ballot_sync(FULL, hf[i] != 0u);
+                    if (fb) j2 = 32 * i + 31 - __clz((int)fb);
+                    const int lim = c - 32 * i;  // lanes below c in this group
+                    const uint32_t lo = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+                    if (fb & lo) j1 = 32 * i + 31 - __clz((int)(fb & lo));
+                }
+                A s_c = (A)0, s_j1 = (A)0, s_j2 = (A)0, s_all = (A)0;
+#pragma unroll
+                for (int i = 0; i < GATHER_LP; ++i) {
+                    const int j = lane + 32 * i;
+                    s_all += tv[i];
+                    if (j < c) s_c += tv[i];
+                    if (j < j1) s_j1 += tv[i];
+                    if (j < j2) s_j2 += tv[i];
+                }
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) {
+                    s_all += shfl_xor(s_all, d);
+                    s_c += shfl_xor(s_c, d);
+                    s_j1 += shfl_xor(s_j1, d);
+                    s_j2 += shfl_xor(s_j2, d);
+                }
+                A h1 = (A)0, h2 = (A)0;
+#pragma unroll
+                for (int i = 0; i < GATHER_LP; ++i) {
+                    if (32 * i >= G) break;
+                    const A v1 = shfl_idx(hv[i], j1 & 31), v2 = shfl_idx(hv[i], j2 & 31);
+                    if ((j1 >> 5) == i) h1 = v1;
+                    if ((j2 >> 5) == i) h2 = v2;
+                }
+                const A mine_pre = s_c, run = s_all;
+                const bool has_before = j1 >= 0, has_last = j2 >= 0;
+                const A head_before = s_j1 + h1, head_last = s_j2 + h2;
+                const A s_start = carry + mine_pre;                        // S at this portion's start
+                const A b_in = has_before ? carry + head_before : bcarry;  // B entering this portion
+                if (lane < NCHUNK) {
+                    chunk_pre[b * MAXC + lane] = s_start + cex;
+                    chunk_B[b * MAXC + lane] = cbelow ? s_start + chead : b_in;
+                }
+                if (has_last) bcarry = carry + head_last;
+                carry += run;
+                __syncwarp();
+                if (lane == 0) SEG_TRACE(r, 5);
+                if (lane == 0) mbar_arrive(&pre[b]);
+            }
+            return;
+        }
+        A carry = (A)0;  // the open segment's running sum at the region start
+        ulonglong2 dn[GATHER_LP];
+        desc_issue(dn, a.desc, G, lane);
+        for (int64_t r = 0; r < a.rounds; ++r) {
+            const int b = (int)(r % NBUF);
+            SEG_WAIT(&red[b], par(r));
+            if (lane == 0) SEG_TRACE(r, 3);
+            // chunk aggregates of this portion: exclusive segmented scan across lanes
+            const Pair cp = lane < NCHUNK ? Pair{chunk_tot[b * MAXC + lane], chunk_f[b * MAXC + lane]} : Pair{(A)0, 0u};
+            const Pair cinc = seg_warp_scan(cp, lane);
+            Pair cex = seg_shfl_up(cinc, 1);
+            if (lane == 0) cex = Pair{(A)0, 0u};
+            // the region's G portion aggregates (flag-masked tag compare)
+            {
+                unsigned pending = 0;
+#pragma unroll
+                for (int i = 0; i < GATHER_LP; ++i)
+                    if (lane + 32 * i < G) pending |= 1u << i;
+                while (true) {
+#pragma unroll
+                    for (int i = 0; i < GATHER_LP; ++i)
+                        if (((pending >> i) & 1) && (dn[i].x & ~(3ull | SEG_FLAG)) == want && (dn[i].x & 3ull) != 0)
+                            pending &= ~(1u << i);
+                    if (!__any_sync(FULL, pending != 0)) break;
+                    __nanosleep(32);
+#pragma unroll
+                    for (int i = 0; i < GATHER_LP; ++i)
+                        if ((pending >> i) & 1) dn[i] = ld_desc(a.desc + r * G + lane + 32 * i);
+                }
+            }
+            if (lane == 0) SEG_TRACE(r, 4);
+            Pair gp[GATHER_LP];
+#pragma unroll
+            for (int i = 0; i < GATHER_LP; ++i)
+                gp[i] = (lane + 32 * i < G) ? Pair{acc_from_bits<A>(dn[i].y), (dn[i].x & SEG_FLAG) ? 1u : 0u}
+                                            : Pair{(A)0, 0u};
+#if PS_SEG_EXP == 1
+#pragma unroll
+            for (int i = 0; i < GATHER_LP; ++i) gp[i].f = 0;
+#endif
+            if (r + 1 < a.rounds) desc_issue(dn, a.desc + (r + 1) * G, G, lane);
+            // segmented scan of the G aggregates in portion order: per group of 32, then groups
+            Pair run{(A)0, 0u}, mine{(A)0, 0u};
+#pragma unroll
+            for (int i = 0; i < GATHER_LP; ++i) {
+                if (32 * i >= G) break;
+                const Pair inc = seg_warp_scan(gp[i], lane);
+                Pair ex = seg_shfl_up(inc, 1);
+                if (lane == 0) ex = Pair{(A)0, 0u};
+                const Pair before = seg_combine(run, ex);
+                if ((c >> 5) == i) mine = before;                     // lane (c & 31) holds this CTA's prefix
+                run = seg_combine(run, Pair{shfl_idx(inc.v, 31), __shfl_sync(FULL, inc.f, 31)});
+            }
+            const Pair cta_ex{shfl_idx(mine.v, c & 31), __shfl_sync(FULL, mine.f, c & 31)};
+            const A portion_in = cta_ex.f ? cta_ex.v : carry + cta_ex.v;
+            if (lane < NCHUNK) chunk_pre[b * MAXC + lane] = cex.f ? cex.v : portion_in + cex.v;
+            carry = run.f ? run.v : carry + run.v;
+            __syncwarp();
+            if (lane == 0) SEG_TRACE(r, 5);
+            if (lane == 0) mbar_arrive(&pre[b]);
+        }
+        return;
+    }
+
+    // ============================== scanners =======================================
+    const uint64_t pol = policy_evict_first();
+    A *tot = reinterpret_cast<A *>(a.totals);
+    for (int64_t r = 0; r < a.rounds; ++r) {
+        const int b = (int)(r % NBUF);
+        SEG_WAIT(&full[b], par(r));
+        SEG_WAIT(&hdr[b], par(r));
+        const TIn *sb = buf + (size_t)b * P;
+        const uint32_t *bm = bitmap + b * BMW;
+        const int32_t *cb = cntb + b * WORDS;
+        const int64_t p0 = p0_of(r);
+        const bool w = whole(r);
+        if (w || live(r)) {
+            const Meta &m = meta[b];  // in shared memory (no local copy)
+            // one lane-row's outputs and, at every head it holds, the total of the segment
+            // that ends just before it (inc[j-1], or the lane's incoming value at j = 0);
+            // the last segment of the input ends at the head at hi (the offset n), which is
+            // inside a boundary portion or, when hi ends a portion, handled by its last lane
+            auto emit = [&](int64_t q0, uint32_t hbits, const A (&inc)[VEC], const TOut (&y)[VEC], A lane_prev) {
+                if (w) {
+                    constexpr int NV = VEC * sizeof(TOut) / 32;
+#pragma unroll
+                    for (int k = 0; k < NV; ++k)
+                        stg256_policy(out + p0 + q0 + k * (32 / sizeof(TOut)), pack<TOut>(&y[k * (32 / sizeof(TOut))]),
+                                      pol);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) {
+                        const int64_t pos = p0 + q0 + j;
+                        if (pos >= a.lo && pos < a.hi) out[pos] = y[j];
+                    }
+                }
+                if (!tot) return;
+                uint32_t heads = hbits;
+                // warp-uniform loop over the (usually single) head of each lane; the value is
+                // picked by selects (static register indices)
+                while (__any_sync(FULL, heads != 0u)) {
+                    const int j = heads ? __ffs((int)heads) - 1 : 0;
+                    A v = lane_prev;
+#pragma unroll
+                    for (int jj = 1; jj < VEC; ++jj)
+                        if (jj == j) v = inc[jj - 1];
+                    if (heads) {
+                        const int64_t x = q0 + j;  // portion position of the head
+                        int64_t sg;
+                        if (!m.dup) {
+                            sg = m.lb0 + cb[x >> 5] + __popc(bm[x >> 5] & ((1u << (x & 31)) - 1u)) - 1;
+                        } else {
+                            const int64_t e = p0 + x - a.lead;  // repeated offsets: lower bound by search
+                            int64_t l = m.lb0, h = m.lb1;
+                            while (l < h) {
+                                const int64_t mid = (l + h) >> 1;
+                                if (__ldg(a.offsets + mid) >= e) h = mid;
+                                else l = mid + 1;
+                            }
+                            sg = l - 1;
+                        }
+                        if (sg >= 0) tot[sg] = v;
+                    }
+                    heads &= heads - 1u;
+                }
+                if (q0 + VEC == P && p0 + P == a.hi && m.next_head) tot[m.lb1 - 1] = inc[VEC - 1];
+            };
+            for (int64_t ch = warp; ch < NCHUNK; ch += SW) {
+                const int64_t c0 = ch * CHUNK;
+                uint32_t hb[ROWS];
+                if constexpr (SUB) {
+                    // one row at a time (a rolled loop keeps the kernel's code small): plain
+                    // in-lane and warp prefix sums as the 1-D stream kernel, then the base B of
+                    // each element's segment -- S before the last head at or before it
+                    if (warp == 0 && lane == 0 && ch == warp) SEG_TRACE(r, 6);
+                    SEG_WAIT(&pre[b], par(r));  // the chunk's S and B (the ledger)
+                    A base = chunk_pre[b * MAXC + ch], bin = chunk_B[b * MAXC + ch];
+#pragma unroll SEG_UNROLL
+                    for (int rr = 0; rr < ROWS; ++rr) {
+                        const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
+                        TIn x[VEC];
+                        if (w) {
+                            unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) {
+                                const int64_t pos = p0 + q0 + j;
+                                x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
+                            }
+                        }
+                        const uint32_t hbr = heads_at(bm, q0);
+                        A run = (A)0, lhl = (A)0;
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            if ((hbr >> j) & 1u) lhl = run;
+                            run += (A)x[j];
+                        }
+                        const uint32_t bh = __ballot_sync(FULL, hbr != 0u);
+                        A sc = run;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const A y = shfl_up(sc, d);
+                            if (lane >= d) sc += y;
+                        }
+                        const A exs = sc - run, rts = shfl_idx(sc, 31);
+                        const A hrel = exs + lhl;  // row-relative S before this lane's last head
+                        const uint32_t below = bh & ((1u << lane) - 1u);
+                        const A hsrc = shfl_idx(hrel, below ? 31 - __clz((int)below) : lane);
+                        A B = below ? base + hsrc : bin;
+                        A S = base + exs;  // S before the lane's first element
+                        const A lane_prev = S - B;
+                        A inc[VEC];
+                        TOut y[VEC];
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            if ((hbr >> j) & 1u) B = S;  // S before the head
+                            y[j] = (TOut)(S - B);       // exclusive value
+                            S += (A)x[j];
+                            inc[j] = S - B;
+                            if (!a.exclusive) y[j] = (TOut)inc[j];
+                        }
+                        emit(q0, hbr, inc, y, lane_prev);
+                        if (bh) bin = base + shfl_idx(hrel, 31 - __clz((int)bh));
+                        base += rts;
+                    }
+                    continue;
+                }
+                A v[ROWS][VEC];
+                Pair ex[ROWS], rt[ROWS];
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) {
+                    const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
+                    TIn x[VEC];
+                    if (w) {
+                        unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            const int64_t pos = p0 + q0 + j;
+                            x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
+                        }
+                    }
+                    hb[rr] = heads_at(bm, q0);
+                    // in-lane segmented prefix: v[j] = sum since the last head at or before j
+                    // (or since the lane's first element if there is none)
+                    A run = (A)0;
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) {
+                        run = ((hb[rr] >> j) & 1u) ? (A)x[j] : run + (A)x[j];
+                        v[rr][j] = run;
+                    }
+                    const Pair inc = seg_warp_scan(Pair{run, hb[rr] != 0u}, lane);
+                    ex[rr] = seg_shfl_up(inc, 1);
+                    if (lane == 0) ex[rr] = Pair{(A)0, 0u};
+                    rt[rr] = Pair{shfl_idx(inc.v, 31), __shfl_sync(FULL, inc.f, 31)};
+                }
+                if (warp == 0 && lane == 0 && ch == 0) SEG_TRACE(r, 6);
+                SEG_WAIT(&pre[b], par(r));  // the chunk carries of region r (the ledger)
+                A base = chunk_pre[b * MAXC + ch];
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) {
+                    const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
+                    const A lane_in = ex[rr].f ? ex[rr].v : base + ex[rr].v;  // sum before the lane's first element
+                    A inc[VEC];
+                    uint32_t seen = 0;
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) {
+                        seen |= (hb[rr] >> j) & 1u;
+                        inc[j] = seen ? v[rr][j] : lane_in + v[rr][j];
+                    }
+                    TOut y[VEC];
+                    if (a.exclusive) {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j)
+                            y[j] = ((hb[rr] >> j) & 1u) ? (TOut)0 : (TOut)(j == 0 ? lane_in : inc[j - 1]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
+                    }
+                    emit(q0, hb[rr], inc, y, lane_in);
+                    base = rt[rr].f ? rt[rr].v : base + rt[rr].v;
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (warp == 0 && lane == 0) SEG_TRACE(r, 7);
+        if (lane == 0) mbar_arrive(&freeb[b]);
+    }
+}
+
+}  // namespace ps

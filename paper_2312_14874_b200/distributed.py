@@ -320,8 +320,9 @@ class DistributedScanEngine:
                 p2 = [(t, Role.INCREMENT, sizes[t]) for t in range(1, g)]
                 launches = 3 if r else 2
                 nbytes = (4 if r else 2) * n * esize
+            # here the two passes and the exchange ARE what ran (one per rank)
             self.last_stats = RunStats(iterations=1, barrier_waits=1, sync_points=2, roles=[(p1, p2)],
-                                       kernel_launches=launches, bytes_moved=nbytes)
+                                       kernel_launches=launches, bytes_moved=nbytes, reference_plan_only=False)
         return total.cpu().item()
 
     def _shard_lengths(self, n_local: int) -> list:

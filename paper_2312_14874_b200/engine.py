@@ -121,10 +121,11 @@ class ScanRequest:
 class RunStats:
     """Per-run instrumentation (engine.py:109-128) plus GPU accounting.
 
-    ``iterations`` / ``barrier_waits`` / ``roles`` describe the plan the
-    reference would have executed for this request (the same
-    ``compute_grid``), so callers comparing schedules keep working;
-    ``kernel_launches`` and ``bytes_moved`` describe what the GPU did."""
+    ``iterations`` / ``barrier_waits`` / ``sync_points`` / ``roles`` are the
+    REFERENCE'S PLAN for this request (the same ``compute_grid``), reported so
+    callers comparing schedules keep working -- the GPU does not execute it
+    (``reference_plan_only`` is True to say so).  What the GPU did is
+    ``kernel_launches`` and ``bytes_moved``."""
 
     iterations: int = 0
     barrier_waits: int = 0
@@ -132,6 +133,7 @@ class RunStats:
     roles: list = field(default_factory=list)
     kernel_launches: int = 0
     bytes_moved: int = 0
+    reference_plan_only: bool = True
 
     def idle_pairs(self, threads: int) -> list:
         pairs = []

@@ -24,7 +24,7 @@ EXTRA_PARAMS = {
 EXTRA_FIELDS = {
     ("bench", "CaseConfig"): {"device"},
     ("bench", "BenchRecord"): {"device", "bandwidth_gbs"},
-    ("engine", "RunStats"): {"kernel_launches", "bytes_moved"},
+    ("engine", "RunStats"): {"kernel_launches", "bytes_moved", "reference_plan_only"},
 }
 # reference entries that are CPU-thread machinery with no GPU counterpart
 NOT_PROVIDED = {("engine", "RunStats", "record"), ("engine", "ScanEngine", "_execute")}
