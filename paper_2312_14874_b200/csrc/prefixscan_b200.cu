@@ -328,7 +328,19 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
 }
 
 // ---- CSR segments on shared-memory regions (seg_stream.cuh) ---------------------------------------
-constexpr int GSW = 8, GROWS = 4, GNBUF = 6, GRWP = 4;
+#ifndef PS_SEG_SW  // geometry overrides for scripts/build_variants.sh experiments
+#define PS_SEG_SW 8
+#endif
+#ifndef PS_SEG_ROWS
+#define PS_SEG_ROWS 4
+#endif
+#ifndef PS_SEG_NBUF
+#define PS_SEG_NBUF 6
+#endif
+#ifndef PS_SEG_RWP
+#define PS_SEG_RWP 4
+#endif
+constexpr int GSW = PS_SEG_SW, GROWS = PS_SEG_ROWS, GNBUF = PS_SEG_NBUF, GRWP = PS_SEG_RWP;
 #define GGEO SegStreamGeom<TIn, GSW, GROWS, GNBUF, GRWP>
 #define GKERN seg_stream_kernel<TIn, TOut, GSW, GROWS, GNBUF, GRWP>
 constexpr int64_t SEG_STREAM_MAX_GRID = STREAM_MAX_GRID;
@@ -405,11 +417,17 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     a.lb = lb;
     a.dupflag = dup;
     a.bitmap = bm;
-    a.totals = totals;
+    using A = typename AccOf<TIn>::type;
+    constexpr bool GATHER = (A)0.5 == (A)0 && sizeof(TOut) == 8;  // totals read back from the output
+    a.totals = GATHER ? nullptr : totals;
+    if (GATHER && totals && exclusive)
+        seg_last_in_kernel<TIn, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
+            static_cast<const TIn *>(in), offsets, nseg, static_cast<A *>(totals));
     a.desc = reinterpret_cast<ulonglong2 *>(sc + 256);
     a.epoch = epoch;
     a.exclusive = exclusive;
     a.inflight = g_tune.stream_inflight;
+    a.one = 1;
     const size_t clear = L.total - L.off_dup;  // repeat flags + bitmap
     cudaError_t e = cudaMemsetAsync(dup, 0, clear, s);
     if (e != cudaSuccess) return cuda_rc(e);
@@ -444,6 +462,9 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
         }
     }
 #endif
+    if (GATHER && totals)
+        seg_totals_gather_kernel<TOut, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
+            static_cast<const TOut *>(out), offsets, nseg, static_cast<A *>(totals), exclusive);
     return cuda_rc(cudaMemsetAsync(dup, 0, clear, s));
 }
 

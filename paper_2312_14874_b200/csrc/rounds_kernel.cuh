@@ -78,6 +78,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, 
         "r"(parity), "r"(hint_ns)
         : "memory");
 }
+// mbarrier wait with a nanosleep back-off between probes (waiting roles leave the issue slots alone)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity, uint32_t ns = 128u) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @p bra DONE_%=;\n"
+        " nanosleep.u32 %2;\n"
+        " bra WAIT_%=;\n DONE_%=:\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

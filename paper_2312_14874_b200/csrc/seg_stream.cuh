@@ -35,10 +35,15 @@
 #ifndef PS_SEG_SLEEP
 #define PS_SEG_SLEEP 1
 #endif
-#if PS_SEG_SLEEP
+#if PS_SEG_SLEEP == 2
+#define SEG_WAIT(bar, par) mbar_wait_backoff(bar, par)
+#elif PS_SEG_SLEEP
 #define SEG_WAIT(bar, par) mbar_wait_sleep(bar, par)
 #else
 #define SEG_WAIT(bar, par) mbar_wait(bar, par)
+#endif
+#ifndef PS_SEG_WIDE
+#define PS_SEG_WIDE 1
 #endif
 #ifndef PS_SEG_UNROLL
 #define PS_SEG_UNROLL 1
@@ -81,6 +86,7 @@ struct SegStreamArgs {
     uint32_t epoch;
     int exclusive;
     int inflight;
+    int one;  // 1 (the opaque multiplier of add_widen)
 };
 
 // Pre-pass, one thread per portion boundary and per offset:
@@ -137,6 +143,68 @@ __global__ void seg_prepare_kernel(const int64_t *off, int64_t nseg, int64_t n, 
         res = lo;
     }
     lb[t] = res << 2;
+}
+
+// Segment totals of the integer instantiations with 64-bit outputs are read back from the
+// scan's own output after the launch (the inclusive value of a segment's last element is its
+// total, exact in two's complement) instead of being scattered by the scanners: one 32-byte
+// sector per segment against a per-head loop on the scanners' serial path.  An exclusive scan
+// keeps the last element in totals[] from before the launch (input and output may alias).
+template <typename TIn, typename A>
+__global__ void seg_last_in_kernel(const TIn *in, const int64_t *off, int64_t nseg, A *tot) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nseg) return;
+    const int64_t b = __ldg(off + t), e = __ldg(off + t + 1);
+    tot[t] = e > b ? (A)in[e - 1] : (A)0;
+}
+template <typename TOut, typename A>
+__global__ void seg_totals_gather_kernel(const TOut *out, const int64_t *off, int64_t nseg, A *tot, int exclusive) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nseg) return;
+    const int64_t b = __ldg(off + t), e = __ldg(off + t + 1);
+    A v = (A)0;
+    if (e > b) {
+        v = (A)out[e - 1];
+        if (exclusive) v += tot[t];
+    }
+    tot[t] = v;
+}
+
+// acc + (A)x.  For 32-bit integer input under a 64-bit accumulator the widening is one
+// IMAD.WIDE on the FMA pipe (multiplier `one` = 1 from the kernel arguments, opaque to
+// ptxas, which would otherwise sign-extend on the ALU pipe): the kernel was bound by the ALU
+// pipe (ncu: 61 % busy against 10 % for the FMA pipe).
+template <typename A, typename TIn> __device__ __forceinline__ A add_widen(A acc, TIn x, int one) {
+#if PS_SEG_WIDE
+    if constexpr (sizeof(TIn) == 4 && sizeof(A) == 8 && (A)0.5 == (A)0) {
+        A d;
+        if constexpr ((TIn)-1 < (TIn)0)
+            asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"((int)x), "r"(one), "l"(acc));
+        else
+            asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"((unsigned)x), "r"(one), "l"(acc));
+        return d;
+    }
+#endif
+    (void)one;
+    return acc + (A)x;
+}
+// inclusive plain scan of a 64-bit integer across the warp: the adds are predicated on
+// shfl.up's own "source lane in range" predicate (no lane compares)
+template <typename A> __device__ __forceinline__ A warp_scan_pred(A v) {
+    static_assert(sizeof(A) == 8, "64-bit accumulators");
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        asm volatile(
+            "{\n .reg .pred q;\n .reg .b32 lo, hi, tl, th;\n .reg .b64 t;\n"
+            " mov.b64 {lo, hi}, %0;\n"
+            " shfl.sync.up.b32 tl|q, lo, %1, 0, 0xffffffff;\n"
+            " shfl.sync.up.b32 th, hi, %1, 0, 0xffffffff;\n"
+            " mov.b64 t, {tl, th};\n"
+            " @q add.s64 %0, %0, t;\n}"
+            : "+l"(v)
+            : "r"(d));
+    }
+    return v;
 }
 
 template <typename A> struct SegPair {
@@ -200,6 +268,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
     // sum and B = S before the last head at or before the element (exact in two's
     // complement); floats: the (flag, value) pair operator (no cancellation)
     constexpr bool SUB = (A)0.5 == (A)0;
+    // integer scans with 64-bit outputs: totals are gathered after the launch (seg_totals_gather_kernel)
+    constexpr bool EMIT = !(SUB && sizeof(TOut) == 8);
     static_assert(32 % VEC == 0, "a lane's head bits sit in one bitmap word");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -354,8 +424,9 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                 for (int64_t ch = rw; ch < NCHUNK; ch += RWP) {
                     A s = (A)0, pl = (A)0;
                     int lastpos = -1;
-                    if (lv) {
+                    if (lv && PS_SEG_EXP != 11) {
                         TIn x[ROWS][VEC];
+                        A rs[ROWS];  // the lane's sum of each row
 #pragma unroll
                         for (int rr = 0; rr < ROWS; ++rr) {
                             const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
@@ -369,25 +440,34 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                                 }
                             }
                             const uint32_t hb = heads_at(bm, q0);
-#if PS_SEG_EXP == 2 || PS_SEG_EXP == 4
-                            (void)hb;
-#else
                             if (hb) lastpos = rr * ROW_ELEMS + lane * VEC + (31 - __clz((int)hb));
-#endif
+                            A t = (A)x[rr][0];
+#pragma unroll
+                            for (int j = 1; j < VEC; ++j) t = add_widen(t, x[rr][j], a.one);
+                            rs[rr] = t;
+                            s += t;
                         }
                         const int lh = __reduce_max_sync(FULL, lastpos);  // the chunk's last head (-1: none)
+                        if (lh >= 0) {
+                            // sum before the last head: whole rows before its row, and in that row
+                            // (warp-uniform index) the elements before it
+                            const int lrow = lh / ROW_ELEMS;
+                            const int lim = lh - lrow * ROW_ELEMS - lane * VEC;  // this lane's elements j < lim
 #pragma unroll
-                        for (int rr = 0; rr < ROWS; ++rr)
+                            for (int rr = 0; rr < ROWS; ++rr) {
+                                if (rr < lrow) {
+                                    pl += rs[rr];
+                                } else if (rr == lrow) {
 #pragma unroll
-                            for (int j = 0; j < VEC; ++j) {
-                                const A v = (A)x[rr][j];
-                                s += v;
-                                if (rr * ROW_ELEMS + lane * VEC + j < lh) pl += v;
+                                    for (int j = 0; j < VEC; ++j)
+                                        if (j < lim) pl += (A)x[rr][j];
+                                }
                             }
+                            pl = warp_sum(pl);
+                        }
                         lastpos = lh;
                     }
                     s = warp_sum(s);
-                    pl = warp_sum(pl);
                     if (lane == 0) {
                         chunk_tot[b * MAXC + ch] = s;
                         chunk_plh[b * MAXC + ch] = pl;
@@ -656,7 +736,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
 
     // ============================== scanners =======================================
     const uint64_t pol = policy_evict_first();
-    A *tot = reinterpret_cast<A *>(a.totals);
+    A *tot = EMIT ? reinterpret_cast<A *>(a.totals) : nullptr;
     for (int64_t r = 0; r < a.rounds; ++r) {
         const int b = (int)(r % NBUF);
         SEG_WAIT(&full[b], par(r));
@@ -672,7 +752,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
             // that ends just before it (inc[j-1], or the lane's incoming value at j = 0);
             // the last segment of the input ends at the head at hi (the offset n), which is
             // inside a boundary portion or, when hi ends a portion, handled by its last lane
-            auto emit = [&](int64_t q0, uint32_t hbits, const A (&inc)[VEC], const TOut (&y)[VEC], A lane_prev) {
+            auto store_row = [&](int64_t q0, const TOut (&y)[VEC]) {
                 if (w) {
                     constexpr int NV = VEC * sizeof(TOut) / 32;
 #pragma unroll
@@ -686,7 +766,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                         if (pos >= a.lo && pos < a.hi) out[pos] = y[j];
                     }
                 }
-                if (!tot) return;
+            };
+            auto emit_totals = [&](int64_t q0, uint32_t hbits, const A (&inc)[VEC], A lane_prev) {
                 uint32_t heads = hbits;
                 // warp-uniform loop over the (usually single) head of each lane; the value is
                 // picked by selects (static register indices)
@@ -715,18 +796,29 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                     }
                     heads &= heads - 1u;
                 }
-                if (q0 + VEC == P && p0 + P == a.hi && m.next_head) tot[m.lb1 - 1] = inc[VEC - 1];
+            };
+            // the input's last segment when hi ends this portion: its total is the last element's value
+            const bool tail_tot = tot && p0 + P == a.hi && m.next_head;
+            auto emit = [&](int64_t q0, uint32_t hbits, const A (&inc)[VEC], const TOut (&y)[VEC], A lane_prev) {
+                store_row(q0, y);
+                if (!tot) return;
+                emit_totals(q0, hbits, inc, lane_prev);
+                if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
             };
             for (int64_t ch = warp; ch < NCHUNK; ch += SW) {
                 const int64_t c0 = ch * CHUNK;
                 uint32_t hb[ROWS];
                 if constexpr (SUB) {
-                    // one row at a time (a rolled loop keeps the kernel's code small): plain
-                    // in-lane and warp prefix sums as the 1-D stream kernel, then the base B of
-                    // each element's segment -- S before the last head at or before it
+                    // one row at a time (a rolled loop: the kernel's hot code has to fit the
+                    // SM's instruction cache, see DESIGN): the plain in-lane and warp prefix sums
+                    // of the 1-D stream kernel give S; a row without heads (warp-uniform test,
+                    // most rows unless segments are short) subtracts one base B for the whole
+                    // row; a row with heads finds each element's base -- S before the last head
+                    // at or before it
                     if (warp == 0 && lane == 0 && ch == warp) SEG_TRACE(r, 6);
                     SEG_WAIT(&pre[b], par(r));  // the chunk's S and B (the ledger)
                     A base = chunk_pre[b * MAXC + ch], bin = chunk_B[b * MAXC + ch];
+                    const int one = a.one;
 #pragma unroll SEG_UNROLL
                     for (int rr = 0; rr < ROWS; ++rr) {
                         const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
@@ -741,38 +833,66 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                             }
                         }
                         const uint32_t hbr = heads_at(bm, q0);
-                        A run = (A)0, lhl = (A)0;
+                        A p[VEC];  // in-lane inclusive prefix
+                        p[0] = (A)x[0];
 #pragma unroll
-                        for (int j = 0; j < VEC; ++j) {
-                            if ((hbr >> j) & 1u) lhl = run;
-                            run += (A)x[j];
-                        }
-                        const uint32_t bh = __ballot_sync(FULL, hbr != 0u);
-                        A sc = run;
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const A y = shfl_up(sc, d);
-                            if (lane >= d) sc += y;
-                        }
-                        const A exs = sc - run, rts = shfl_idx(sc, 31);
-                        const A hrel = exs + lhl;  // row-relative S before this lane's last head
-                        const uint32_t below = bh & ((1u << lane) - 1u);
-                        const A hsrc = shfl_idx(hrel, below ? 31 - __clz((int)below) : lane);
-                        A B = below ? base + hsrc : bin;
-                        A S = base + exs;  // S before the lane's first element
-                        const A lane_prev = S - B;
-                        A inc[VEC];
+                        for (int j = 1; j < VEC; ++j) p[j] = add_widen(p[j - 1], x[j], one);
+                        const uint32_t bh = PS_SEG_EXP == 12 ? 0u : __ballot_sync(FULL, hbr != 0u);
+                        const A sc = warp_scan_pred(p[VEC - 1]);
+                        const A exs = sc - p[VEC - 1], rts = shfl_idx(sc, 31);
                         TOut y[VEC];
+                        if (bh == 0u) {
+                            const A d = base + exs - bin;  // the open segment's sum before this lane
+                            if (a.exclusive) {
+                                y[0] = (TOut)d;
 #pragma unroll
-                        for (int j = 0; j < VEC; ++j) {
-                            if ((hbr >> j) & 1u) B = S;  // S before the head
-                            y[j] = (TOut)(S - B);       // exclusive value
-                            S += (A)x[j];
-                            inc[j] = S - B;
-                            if (!a.exclusive) y[j] = (TOut)inc[j];
+                                for (int j = 1; j < VEC; ++j) y[j] = (TOut)(d + p[j - 1]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j) y[j] = (TOut)(d + p[j]);
+                            }
+                            store_row(q0, y);
+                            if constexpr (EMIT)
+                                if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = d + p[VEC - 1];
+                        } else {
+                            // o[j]: the sum since the lane's last head at or before j (since the
+                            // lane's start before its first head); pb: the lane's sum before its last head
+                            A pb = (A)0, o[VEC];
+                            o[0] = p[0];
+#pragma unroll
+                            for (int j = 1; j < VEC; ++j) {
+                                if ((hbr >> j) & 1u) pb = p[j - 1];
+                                o[j] = p[j] - pb;
+                            }
+                            const A hrel = exs + pb;  // row-relative S before this lane's last head
+                            const uint32_t below = bh & ((1u << lane) - 1u);
+                            const A hsrc = shfl_idx(hrel, below ? 31 - __clz((int)below) : lane);
+                            const A Bl = below ? base + hsrc : bin;
+                            const A d = base + exs - Bl;
+                            A inc[VEC];
+                            uint32_t seen = 0;
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) {
+                                seen |= (hbr >> j) & 1u;
+                                inc[j] = seen ? o[j] : d + p[j];
+                            }
+                            if (a.exclusive) {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j)
+                                    y[j] = ((hbr >> j) & 1u) ? (TOut)0 : (TOut)(j == 0 ? d : inc[j - 1]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
+                            }
+                            store_row(q0, y);
+                            if constexpr (EMIT) {
+                                if (tot) {
+                                    emit_totals(q0, hbr, inc, d);
+                                    if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                                }
+                            }
+                            bin = base + shfl_idx(hrel, 31 - __clz((int)bh));
                         }
-                        emit(q0, hbr, inc, y, lane_prev);
-                        if (bh) bin = base + shfl_idx(hrel, 31 - __clz((int)bh));
                         base += rts;
                     }
                     continue;
