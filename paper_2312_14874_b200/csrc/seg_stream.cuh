@@ -45,6 +45,15 @@
 #ifndef PS_SEG_WIDE
 #define PS_SEG_WIDE 1
 #endif
+#ifndef PS_SEG_RED_ROLLED
+#define PS_SEG_RED_ROLLED 0
+#endif
+#ifndef PS_SEG_POLL_NS  // ledger: pause between polls of a region's descriptors
+#define PS_SEG_POLL_NS 32
+#endif
+#ifndef PS_SEG_EARLY_ISSUE
+#define PS_SEG_EARLY_ISSUE 0
+#endif
 #ifndef PS_SEG_UNROLL
 #define PS_SEG_UNROLL 1
 #endif
@@ -244,7 +253,8 @@ struct SegStreamGeom {
     static constexpr int WORDS = (int)(P / 32);         // head bitmap words per portion
     static constexpr int BMW = WORDS + 4;               // per slot: + the next 128 positions (TMA: 16 B units)
     using Meta = SegMeta;
-    static constexpr int SMEM_FIXED = NBUF * BMW * 4 + 5 * NBUF * 8 + 4 * NBUF * MAXC * 8 + NBUF * MAXC * 4 +
+    static constexpr int SMEM_FIXED = NBUF * BMW * 4 + 5 * NBUF * 8 + 4 * NBUF * MAXC * 8 + 2 * 32 * GATHER_LP * 8 + 32 * GATHER_LP * 4 +
+                                      2 * NBUF * MAXC * 4 +
                                       NBUF * WORDS * 4 + NBUF * (int)sizeof(Meta) + 128;
     static constexpr int SMEM = (int)(NBUF * P * sizeof(TIn)) + SMEM_FIXED;
 };
@@ -285,8 +295,12 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
     A *chunk_pre = chunk_tot + NBUF * MAXC;
     A *chunk_plh = chunk_pre + NBUF * MAXC;  // SUB: chunk sum before its last head (reducers)
     A *chunk_B = chunk_plh + NBUF * MAXC;    // SUB: S before the last head preceding the chunk (ledger)
-    uint32_t *chunk_f = reinterpret_cast<uint32_t *>(chunk_B + NBUF * MAXC);
-    int32_t *cntb = reinterpret_cast<int32_t *>(chunk_f + NBUF * MAXC);
+    A *led_S = chunk_B + NBUF * MAXC;          // SUB ledger: S at the start of every portion of the region
+    A *led_H = led_S + 32 * GATHER_LP;         // ... and S before every portion's last head
+    uint32_t *led_F = reinterpret_cast<uint32_t *>(led_H + 32 * GATHER_LP);  // transposition: head flags
+    uint32_t *chunk_f = led_F + 32 * GATHER_LP;
+    int32_t *chunk_lh = reinterpret_cast<int32_t *>(chunk_f + NBUF * MAXC);  // chunk-relative last head, -1: none (head warp)
+    int32_t *cntb = chunk_lh + NBUF * MAXC;
     Meta *meta = reinterpret_cast<Meta *>(cntb + NBUF * WORDS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -374,22 +388,38 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
             SEG_WAIT(&full[b], par(r));  // the bitmap slice has landed
             const uint32_t *bm = bitmap + b * BMW;
             int32_t *cb = cntb + b * WORDS;
-            // heads before each 32-position word: exclusive scan of popcounts
-            int32_t v[PER], run = 0;
+            // lane k holds the bitmap words of row k of the portion (32 rows): the last head of
+            // every chunk (ROWS consecutive rows), for the reducers and the ledger
+            static_assert(PER * 32 == ROW_ELEMS, "one lane of the head warp per row");
+            uint32_t wd[PER];
+            int32_t last = -1;
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
-                v[j] = run;
-                run += __popc(bm[lane * PER + j]);
+                wd[j] = bm[lane * PER + j];
+                if (wd[j]) last = (lane * PER + j) * 32 + (31 - __clz((int)wd[j]));
             }
-            int32_t incl = run;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int32_t y = __shfl_up_sync(FULL, incl, d);
-                if (lane >= d) incl += y;
+            for (int d = 1; d < ROWS; d <<= 1) last = max(last, __shfl_xor_sync(FULL, last, d));
+            if (lane % ROWS == 0 && lane / ROWS < NCHUNK)
+                chunk_lh[b * MAXC + lane / ROWS] = last >= 0 ? last - (lane / ROWS) * CHUNK : -1;
+            if constexpr (EMIT) {
+                // heads before each 32-position word: exclusive scan of popcounts
+                int32_t v[PER], run = 0;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    v[j] = run;
+                    run += __popc(wd[j]);
+                }
+                int32_t incl = run;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int32_t y = __shfl_up_sync(FULL, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                const int32_t ex = incl - run;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) cb[lane * PER + j] = ex + v[j];
             }
-            const int32_t ex = incl - run;
-#pragma unroll
-            for (int j = 0; j < PER; ++j) cb[lane * PER + j] = ex + v[j];
             if (lane == 0) {
                 Meta m;
                 m.lb0 = s0;
@@ -424,6 +454,49 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                 for (int64_t ch = rw; ch < NCHUNK; ch += RWP) {
                     A s = (A)0, pl = (A)0;
                     int lastpos = -1;
+#if PS_SEG_RED_ROLLED
+                    if (lv && PS_SEG_EXP != 11) {
+                        // the chunk's last head from the head bitmap alone, then one rolled pass
+                        // over the rows (small code: the hot loops of all roles share the SM's
+                        // instruction cache)
+#pragma unroll
+                        for (int rr = 0; rr < ROWS; ++rr) {
+                            const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
+                            const uint32_t hb = heads_at(bm, q0);
+                            if (hb) lastpos = rr * ROW_ELEMS + lane * VEC + (31 - __clz((int)hb));
+                        }
+                        const int lh = __reduce_max_sync(FULL, lastpos);  // -1: none
+                        const int lrow = lh >= 0 ? lh / ROW_ELEMS : -1;
+                        const int lim = lh - lrow * ROW_ELEMS - lane * VEC;  // row lrow: this lane's elements j < lim
+#pragma unroll 1
+                        for (int rr = 0; rr < ROWS; ++rr) {
+                            const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
+                            TIn x[VEC];
+                            if (w) {
+                                unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j) {
+                                    const int64_t pos = p0 + q0 + j;
+                                    x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
+                                }
+                            }
+                            A t = (A)x[0];
+#pragma unroll
+                            for (int j = 1; j < VEC; ++j) t = add_widen(t, x[j], a.one);
+                            s += t;
+                            if (rr < lrow) {
+                                pl += t;
+                            } else if (rr == lrow) {
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j)
+                                    if (j < lim) pl += (A)x[j];
+                            }
+                        }
+                        if (lh >= 0) pl = warp_sum(pl);
+                        lastpos = lh;
+                    }
+#else
                     if (lv && PS_SEG_EXP != 11) {
                         TIn x[ROWS][VEC];
                         A rs[ROWS];  // the lane's sum of each row
@@ -439,15 +512,15 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                                     x[rr][j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
                                 }
                             }
-                            const uint32_t hb = heads_at(bm, q0);
-                            if (hb) lastpos = rr * ROW_ELEMS + lane * VEC + (31 - __clz((int)hb));
                             A t = (A)x[rr][0];
 #pragma unroll
-                            for (int j = 1; j < VEC; ++j) t = add_widen(t, x[rr][j], a.one);
+                            for (int j = 1; j < VEC; ++j)
+                                if (PS_SEG_EXP != 15 || j == VEC - 1) t = add_widen(t, x[rr][j], a.one);
                             rs[rr] = t;
                             s += t;
                         }
-                        const int lh = __reduce_max_sync(FULL, lastpos);  // the chunk's last head (-1: none)
+                        SEG_WAIT(&hdr[b], par(r));  // the head warp's pass over the slot's bitmap
+                        const int lh = PS_SEG_EXP == 16 ? -1 : chunk_lh[b * MAXC + ch];  // the chunk's last head (-1: none)
                         if (lh >= 0) {
                             // sum before the last head: whole rows before its row, and in that row
                             // (warp-uniform index) the elements before it
@@ -467,6 +540,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                         }
                         lastpos = lh;
                     }
+#endif
                     s = warp_sum(s);
                     if (lane == 0) {
                         chunk_tot[b * MAXC + ch] = s;
@@ -556,12 +630,28 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
         // ============================ ledger =====================================
         if constexpr (SUB) {
             // plain carries as the 1-D stream kernel, plus the running sum before the last
-            // head seen so far (B), region by region
+            // head seen so far (B), region by region.  Lane l holds GATHER_LP *consecutive*
+            // portions (l * GATHER_LP + i): their in-lane prefix plus ONE warp scan of the lane
+            // totals gives S at the start of every portion; the three lookups (this CTA's
+            // portion, the last head-holding portion before it, the region's last one) go
+            // through a small shared array.  (The first version kept portions lane + 32 i and
+            // took four masked sums with butterfly reductions plus per-group shuffles: ~300
+            // dependent instructions, 1.3-1.5 us per region -- the kernel's critical loop.)
+            constexpr int LP = GATHER_LP;
             ulonglong2 *desc2 = a.desc + a.rounds * G;
             A carry = (A)0, bcarry = (A)0;
-            ulonglong2 dn[GATHER_LP], dh[GATHER_LP];
-            desc_issue(dn, a.desc, G, lane);
-            desc_issue(dh, desc2, G, lane);
+            ulonglong2 dn[LP], dh[LP];
+            auto issue = [&](int64_t r) {
+#pragma unroll
+                for (int i = 0; i < LP; ++i) {
+                    const int j = lane + 32 * i;  // coalesced polls; transposed through shared memory below
+                    if (j < G) {
+                        dn[i] = ld_desc(a.desc + r * G + j);
+                        dh[i] = ld_desc(desc2 + r * G + j);
+                    }
+                }
+            };
+            issue(0);
             for (int64_t r = 0; r < a.rounds; ++r) {
                 const int b = (int)(r % NBUF);
                 SEG_WAIT(&red[b], par(r));
@@ -585,18 +675,18 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                 {
                     unsigned pending = 0;
 #pragma unroll
-                    for (int i = 0; i < GATHER_LP; ++i)
+                    for (int i = 0; i < LP; ++i)
                         if (lane + 32 * i < G) pending |= 1u << i;
                     while (true) {
 #pragma unroll
-                        for (int i = 0; i < GATHER_LP; ++i)
+                        for (int i = 0; i < LP; ++i)
                             if (((pending >> i) & 1) && (dn[i].x & ~3ull) == want && (dn[i].x & 3ull) != 0 &&
                                 (dh[i].x & ~(3ull | SEG_FLAG)) == want && (dh[i].x & 3ull) != 0)
                                 pending &= ~(1u << i);
                         if (!__any_sync(FULL, pending != 0)) break;
-                        __nanosleep(32);
+                        __nanosleep(PS_SEG_POLL_NS);
 #pragma unroll
-                        for (int i = 0; i < GATHER_LP; ++i)
+                        for (int i = 0; i < LP; ++i)
                             if ((pending >> i) & 1) {
                                 dn[i] = ld_desc(a.desc + r * G + lane + 32 * i);
                                 dh[i] = ld_desc(desc2 + r * G + lane + 32 * i);
@@ -604,58 +694,46 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                     }
                 }
                 if (lane == 0) SEG_TRACE(r, 4);
-                A tv[GATHER_LP], hv[GATHER_LP];
-                uint32_t hf[GATHER_LP];
+                // transpose: lane l takes the LP consecutive portions l * LP + i
 #pragma unroll
-                for (int i = 0; i < GATHER_LP; ++i) {
-                    const bool ok = lane + 32 * i < G;
-                    tv[i] = ok ? acc_from_bits<A>(dn[i].y) : (A)0;
-                    hv[i] = ok ? acc_from_bits<A>(dh[i].y) : (A)0;
-                    hf[i] = ok && (dh[i].x & SEG_FLAG) ? 1u : 0u;
-                }
-                if (r + 1 < a.rounds) {
-                    desc_issue(dn, a.desc + (r + 1) * G, G, lane);
-                    desc_issue(dh, desc2 + (r + 1) * G, G, lane);
-                }
-                // no scan over the G portions is needed, only masked sums: S at this CTA's
-                // portion (sum of the totals before c), at the last head-holding portion before
-                // c (j1) and at the last one of the region (j2), and the region total
-                int j1 = -1, j2 = -1;
-#pragma unroll
-                for (int i = 0; i < GATHER_LP; ++i) {
-                    const uint32_t fb = __ballot_sync(FULL, hf[i] != 0u);
-                    if (fb) j2 = 32 * i + 31 - __clz((int)fb);
-                    const int lim = c - 32 * i;  // lanes below c in this group
-                    const uint32_t lo = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
-                    if (fb & lo) j1 = 32 * i + 31 - __clz((int)(fb & lo));
-                }
-                A s_c = (A)0, s_j1 = (A)0, s_j2 = (A)0, s_all = (A)0;
-#pragma unroll
-                for (int i = 0; i < GATHER_LP; ++i) {
+                for (int i = 0; i < LP; ++i) {
                     const int j = lane + 32 * i;
-                    s_all += tv[i];
-                    if (j < c) s_c += tv[i];
-                    if (j < j1) s_j1 += tv[i];
-                    if (j < j2) s_j2 += tv[i];
+                    led_S[j] = j < G ? acc_from_bits<A>(dn[i].y) : (A)0;
+                    led_H[j] = j < G ? acc_from_bits<A>(dh[i].y) : (A)0;
+                    led_F[j] = j < G && (dh[i].x & SEG_FLAG) ? 1u : 0u;
                 }
+                __syncwarp();
+                A sbef[LP], hv[LP];  // in-lane: sum of the lane's portions before i; sum before portion i's last head
+                A run = (A)0;
+                int best1 = -1, best2 = -1;  // last head-holding portion before c / of the region, among this lane's
 #pragma unroll
-                for (int d = 16; d > 0; d >>= 1) {
-                    s_all += shfl_xor(s_all, d);
-                    s_c += shfl_xor(s_c, d);
-                    s_j1 += shfl_xor(s_j1, d);
-                    s_j2 += shfl_xor(s_j2, d);
+                for (int i = 0; i < LP; ++i) {
+                    const int j = lane * LP + i;
+                    sbef[i] = run;
+                    run += led_S[j];
+                    hv[i] = led_H[j];
+                    if (led_F[j]) {
+                        best2 = j;
+                        if (j < c) best1 = j;
+                    }
                 }
-                A h1 = (A)0, h2 = (A)0;
+                __syncwarp();
+#if PS_SEG_EARLY_ISSUE
+                if (r + 1 < a.rounds) issue(r + 1);
+#endif
+                const A incl = warp_scan_pred(run);
+                const A excl = incl - run, s_all = shfl_idx(incl, 31);
+                const int j1 = __reduce_max_sync(FULL, best1), j2 = __reduce_max_sync(FULL, best2);
 #pragma unroll
-                for (int i = 0; i < GATHER_LP; ++i) {
-                    if (32 * i >= G) break;
-                    const A v1 = shfl_idx(hv[i], j1 & 31), v2 = shfl_idx(hv[i], j2 & 31);
-                    if ((j1 >> 5) == i) h1 = v1;
-                    if ((j2 >> 5) == i) h2 = v2;
+                for (int i = 0; i < LP; ++i) {
+                    const A sp = excl + sbef[i];  // S (region-relative) at the start of portion l * LP + i
+                    led_S[lane * LP + i] = sp;
+                    led_H[lane * LP + i] = sp + hv[i];
                 }
-                const A mine_pre = s_c, run = s_all;
+                __syncwarp();
+                const A mine_pre = led_S[c], run_all = s_all;
                 const bool has_before = j1 >= 0, has_last = j2 >= 0;
-                const A head_before = s_j1 + h1, head_last = s_j2 + h2;
+                const A head_before = has_before ? led_H[j1] : (A)0, head_last = has_last ? led_H[j2] : (A)0;
                 const A s_start = carry + mine_pre;                        // S at this portion's start
                 const A b_in = has_before ? carry + head_before : bcarry;  // B entering this portion
                 if (lane < NCHUNK) {
@@ -663,10 +741,15 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                     chunk_B[b * MAXC + lane] = cbelow ? s_start + chead : b_in;
                 }
                 if (has_last) bcarry = carry + head_last;
-                carry += run;
+                carry += run_all;
                 __syncwarp();
                 if (lane == 0) SEG_TRACE(r, 5);
                 if (lane == 0) mbar_arrive(&pre[b]);
+#if !PS_SEG_EARLY_ISSUE
+                // the next region's gather only now: its pending loads would hold the scoreboards
+                // the fold's shuffles wait on (measured: the fold then takes one L2 round trip)
+                if (r + 1 < a.rounds) issue(r + 1);
+#endif
             }
             return;
         }
@@ -694,7 +777,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                         if (((pending >> i) & 1) && (dn[i].x & ~(3ull | SEG_FLAG)) == want && (dn[i].x & 3ull) != 0)
                             pending &= ~(1u << i);
                     if (!__any_sync(FULL, pending != 0)) break;
-                    __nanosleep(32);
+                    __nanosleep(PS_SEG_POLL_NS);
 #pragma unroll
                     for (int i = 0; i < GATHER_LP; ++i)
                         if ((pending >> i) & 1) dn[i] = ld_desc(a.desc + r * G + lane + 32 * i);
@@ -753,6 +836,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
             // the last segment of the input ends at the head at hi (the offset n), which is
             // inside a boundary portion or, when hi ends a portion, handled by its last lane
             auto store_row = [&](int64_t q0, const TOut (&y)[VEC]) {
+                if (PS_SEG_EXP == 13 && a.exclusive != 77) return;  // ablation: no output stores
                 if (w) {
                     constexpr int NV = VEC * sizeof(TOut) / 32;
 #pragma unroll
@@ -838,8 +922,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
 #pragma unroll
                         for (int j = 1; j < VEC; ++j) p[j] = add_widen(p[j - 1], x[j], one);
                         const uint32_t bh = PS_SEG_EXP == 12 ? 0u : __ballot_sync(FULL, hbr != 0u);
-                        const A sc = warp_scan_pred(p[VEC - 1]);
-                        const A exs = sc - p[VEC - 1], rts = shfl_idx(sc, 31);
+                        const A sc = PS_SEG_EXP == 14 ? p[VEC - 1] * (lane + 1) : warp_scan_pred(p[VEC - 1]);  // 14: ablation
+                        const A exs = sc - p[VEC - 1], rts = PS_SEG_EXP == 14 ? sc + lane : shfl_idx(sc, 31);
                         TOut y[VEC];
                         if (bh == 0u) {
                             const A d = base + exs - bin;  // the open segment's sum before this lane
