@@ -77,7 +77,10 @@ def main():
     data[cfg] = {"dram_bytes_per_launch": traffic, "kernel": dominant, "source": f"profiles/{tag}_{cfg}_launches.md"}
     json.dump(data, open(tj, "w"), indent=1)
     if full:
-        raw = subprocess.run(["ncu", "-i", full, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        if full.endswith(".csv"):  # already exported on the GPU box (`ncu -i x.ncu-rep --page raw --csv`)
+            raw = open(full).read()
+        else:
+            raw = subprocess.run(["ncu", "-i", full, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(raw.splitlines()))
         head, units, vals = rows[0], rows[1], rows[2]
         out = [f"# {tag} {cfg}: `ncu --set full` of `{vals[head.index('Kernel Name')]}`", "",

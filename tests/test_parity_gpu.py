@@ -828,6 +828,32 @@ def test_cfg5_full_properties(ps):
         assert np.array_equal(out[a:a + (1 << 20)].cpu().numpy(), np.cumsum(w) + carry)
 
 
+def test_cfg5_baseline_draw_bit_exact(ps):
+    """cfg5 on the exact BASELINE.json draw (np.random.default_rng(4), 2^31 int64 in
+    [0, 1000]): the whole output chunk-wise against np.cumsum continued with the carry
+    (== the reference's `_scan_kernel`, core.py:86-92, below 2^53) and the returned total
+    against the value the survey recorded from the reference itself."""
+    import psutil
+    import bench
+    from paper_2312_14874_b200 import device
+    if torch.cuda.get_device_properties(0).total_memory < 40 * 2**30:
+        pytest.skip("needs > 40 GB of device memory")
+    if psutil.virtual_memory().available < 24 * 2**30:
+        pytest.skip("needs 16 GiB of host memory for the BASELINE draw")
+    cfg = bench.CONFIGS["cfg5"]
+    xh = bench.host_input(cfg)
+    assert xh.shape == (2**31,) and xh.dtype == np.int64
+    x = torch.empty(2**31, dtype=torch.int64, device="cuda")
+    step = 1 << 28
+    for a in range(0, 2**31, step):
+        x[a:a + step].copy_(torch.from_numpy(xh[a:a + step]))
+    out = torch.empty_like(x)
+    total = device.scan(x, out)
+    assert int(total.item()) == bench.KNOWN_TOTALS["cfg5"] == 1073746006907
+    res = bench.verify_host(cfg, xh, out)  # raises on the first differing element
+    assert res["bit_exact"] and res["total"] == 1073746006907
+
+
 def test_cuda_graph_replays(ps):
     """Scans captured in a CUDA graph and replayed several times over changing input
     contents: every replay starts from a zeroed scratch (the epochs are baked into the
