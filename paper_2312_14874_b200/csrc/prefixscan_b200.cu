@@ -420,6 +420,10 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     using A = typename AccOf<TIn>::type;
     constexpr bool GATHER = (A)0.5 == (A)0 && sizeof(TOut) == 8;  // totals read back from the output
     a.totals = GATHER ? nullptr : totals;
+    if (!GATHER && totals) {  // emitted by the scanners: empty segments keep the zero
+        cudaError_t ze = cudaMemsetAsync(totals, 0, (size_t)nseg * 8, s);
+        if (ze != cudaSuccess) return cuda_rc(ze);
+    }
     if (GATHER && totals && exclusive)
         seg_last_in_kernel<TIn, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
             static_cast<const TIn *>(in), offsets, nseg, static_cast<A *>(totals));
@@ -462,6 +466,12 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
         }
     }
 #endif
+    if (GATHER && PS_SEG_INCLEAR) {  // these instantiations cleared the repeat flags and the bitmap as they consumed them
+        if (totals)
+            seg_totals_gather_kernel<TOut, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
+                static_cast<const TOut *>(out), offsets, nseg, static_cast<A *>(totals), exclusive);
+        return launch_rc();
+    }
     if (GATHER && totals)
         seg_totals_gather_kernel<TOut, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
             static_cast<const TOut *>(out), offsets, nseg, static_cast<A *>(totals), exclusive);
@@ -1033,11 +1043,12 @@ int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_o
     if (epoch == 0 || epoch > PS_EPOCH_MAX) return PS_ERR_EPOCH;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (nseg == 0) return PS_OK;
-    if (seg_totals) {
-        cudaError_t e = cudaMemsetAsync(seg_totals, 0, (size_t)nseg * 8, s);
-        if (e != cudaSuccess) return cuda_rc(e);
-    }
-    if (n == 0) return PS_OK;
+    // totals start from zero (empty segments keep it) -- except where the region kernel's
+    // gather pass writes every entry itself (launch_seg_stream)
+    auto zero_totals = [&]() -> int {
+        return seg_totals ? cuda_rc(cudaMemsetAsync(seg_totals, 0, (size_t)nseg * 8, s)) : PS_OK;
+    };
+    if (n == 0) return zero_totals();
     if (overlaps_partially(in, (size_t)n * dsize(dtype_in), out, (size_t)n * dsize(dtype_out))) return PS_ERR_OVERLAP;
     if (in == out && dsize(dtype_in) != dsize(dtype_out)) return PS_ERR_OVERLAP;
     if (!scratch || scratch_bytes < seg_scratch_bytes(n, (int)dsize(dtype_in))) return PS_ERR_SCRATCH;
@@ -1052,6 +1063,7 @@ int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_o
                                                      scratch, scratch_bytes, epoch, s);                        \
             if (rc >= 0) return rc;                                                                            \
         }                                                                                                      \
+        if (const int zrc = zero_totals()) return zrc;                                                         \
         return launch_segmented<TI, TO>(in, out, n, seg_offsets, nseg, exclusive, seg_totals, scratch, epoch, s); \
     }
     PS_DISPATCH_PAIR(dtype_in, dtype_out, CALL);

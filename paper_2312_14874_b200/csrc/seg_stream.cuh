@@ -54,6 +54,15 @@
 #ifndef PS_SEG_EARLY_ISSUE
 #define PS_SEG_EARLY_ISSUE 0
 #endif
+#ifndef PS_SEG_WSPLIT  // scanner: separate copy of the row loop for whole portions
+#define PS_SEG_WSPLIT 1
+#endif
+#ifndef PS_SEG_INCLEAR  // head warp clears the consumed bitmap slice (no memset after the launch)
+#define PS_SEG_INCLEAR 1
+#endif
+#ifndef PS_SEG_RED_WSPLIT  // reducers: separate whole-portion copy (measured slower: code layout)
+#define PS_SEG_RED_WSPLIT 0
+#endif
 #ifndef PS_SEG_UNROLL
 #define PS_SEG_UNROLL 1
 #endif
@@ -70,6 +79,8 @@ __device__ uint64_t *g_seg_trace;
 #else
 #define SEG_TRACE(r, k) do { } while (0)
 #endif
+
+#include <type_traits>
 
 #include "stream_kernel.cuh"
 
@@ -254,7 +265,7 @@ struct SegStreamGeom {
     static constexpr int BMW = WORDS + 4;               // per slot: + the next 128 positions (TMA: 16 B units)
     using Meta = SegMeta;
     static constexpr int SMEM_FIXED = NBUF * BMW * 4 + 5 * NBUF * 8 + 4 * NBUF * MAXC * 8 + 2 * 32 * GATHER_LP * 8 + 32 * GATHER_LP * 4 +
-                                      2 * NBUF * MAXC * 4 +
+                                      2 * NBUF * MAXC * 4 + NBUF * 4 +
                                       NBUF * WORDS * 4 + NBUF * (int)sizeof(Meta) + 128;
     static constexpr int SMEM = (int)(NBUF * P * sizeof(TIn)) + SMEM_FIXED;
 };
@@ -300,7 +311,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
     uint32_t *led_F = reinterpret_cast<uint32_t *>(led_H + 32 * GATHER_LP);  // transposition: head flags
     uint32_t *chunk_f = led_F + 32 * GATHER_LP;
     int32_t *chunk_lh = reinterpret_cast<int32_t *>(chunk_f + NBUF * MAXC);  // chunk-relative last head, -1: none (head warp)
-    int32_t *cntb = chunk_lh + NBUF * MAXC;
+    uint32_t *row_heads = reinterpret_cast<uint32_t *>(chunk_lh + NBUF * MAXC);  // per slot: bit k = row k holds a head
+    int32_t *cntb = reinterpret_cast<int32_t *>(row_heads + NBUF);
     Meta *meta = reinterpret_cast<Meta *>(cntb + NBUF * WORDS);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -338,10 +350,24 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
 
     if (warp == W_PROD) {
         // ============================ producer ===================================
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            for (int64_t r = 0; r < a.rounds; ++r) {
-                const int b = (int)(r % NBUF);
+        // lane 0 issues the bulk copies; for the instantiations whose totals are gathered
+        // (nothing reads a neighbour's head bits) the whole warp also clears the global
+        // bitmap slice and repeat flag of a region once its slot has been released, so the
+        // launch leaves the scratch clean without a 32 MB memset behind it
+        constexpr bool CLEAR = !EMIT && PS_SEG_INCLEAR;
+        auto clear_region = [&](int64_t r) {
+            uint32_t *g = const_cast<uint32_t *>(a.bitmap) + (p0_of(r) >> 5);
+            for (int k = lane * 4; k < WORDS; k += 128) *reinterpret_cast<uint4 *>(g + k) = make_uint4(0u, 0u, 0u, 0u);
+            if (lane == 0) const_cast<uint32_t *>(a.dupflag)[r * G + c] = 0u;
+            if (r == a.rounds - 1 && c == G - 1 && lane == 1) {  // past the last portion
+                *reinterpret_cast<uint4 *>(g + WORDS) = make_uint4(0u, 0u, 0u, 0u);
+                const_cast<uint32_t *>(a.dupflag)[a.rounds * G] = 0u;
+            }
+        };
+        const uint64_t pol = policy_evict_first();
+        for (int64_t r = 0; r < a.rounds; ++r) {
+            const int b = (int)(r % NBUF);
+            if (lane == 0) {
                 if (r >= NBUF) SEG_WAIT(&freeb[b], par(r - NBUF));
                 if (r >= a.inflight && a.inflight > 0 && a.inflight < NBUF)
                     SEG_WAIT(&full[(r - a.inflight) % NBUF], par(r - a.inflight));
@@ -360,6 +386,17 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                     for (uint32_t o = 0; o < bytes; o += PIECE)
                         bulk_g2s(dst + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, &full[b], pol);
                 }
+            }
+            if constexpr (CLEAR) {
+                __syncwarp();  // lane 0 has seen slot b released: region r - NBUF is done with
+                if (r >= NBUF) clear_region(r - NBUF);
+            }
+        }
+        if constexpr (CLEAR) {
+            for (int64_t r = a.rounds > NBUF ? a.rounds - NBUF : 0; r < a.rounds; ++r) {
+                if (lane == 0) SEG_WAIT(&freeb[r % NBUF], par(r));
+                __syncwarp();
+                clear_region(r);
             }
         }
         return;
@@ -398,6 +435,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                 wd[j] = bm[lane * PER + j];
                 if (wd[j]) last = (lane * PER + j) * 32 + (31 - __clz((int)wd[j]));
             }
+            const uint32_t rowmask = __ballot_sync(FULL, last >= 0);
+            if (lane == 0) row_heads[b] = rowmask;
 #pragma unroll
             for (int d = 1; d < ROWS; d <<= 1) last = max(last, __shfl_xor_sync(FULL, last, d));
             if (lane % ROWS == 0 && lane / ROWS < NCHUNK)
@@ -497,13 +536,14 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                         lastpos = lh;
                     }
 #else
-                    if (lv && PS_SEG_EXP != 11) {
+                    auto reduce_chunk = [&](auto whole_c) {
+                        constexpr bool W = decltype(whole_c)::value;
                         TIn x[ROWS][VEC];
                         A rs[ROWS];  // the lane's sum of each row
 #pragma unroll
                         for (int rr = 0; rr < ROWS; ++rr) {
                             const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
-                            if (w) {
+                            if (W || w) {
                                 unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x[rr]);
                             } else {
 #pragma unroll
@@ -539,6 +579,14 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                             pl = warp_sum(pl);
                         }
                         lastpos = lh;
+                    };
+                    if (lv && PS_SEG_EXP != 11) {
+#if PS_SEG_RED_WSPLIT
+                        if (w) reduce_chunk(std::true_type{});  // whole portions: no bounds logic in the hot copy
+                        else reduce_chunk(std::false_type{});
+#else
+                        reduce_chunk(std::false_type{});
+#endif
                     }
 #endif
                     s = warp_sum(s);
@@ -895,90 +943,113 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                 if constexpr (SUB) {
                     // one row at a time (a rolled loop: the kernel's hot code has to fit the
                     // SM's instruction cache, see DESIGN): the plain in-lane and warp prefix sums
-                    // of the 1-D stream kernel give S; a row without heads (warp-uniform test,
-                    // most rows unless segments are short) subtracts one base B for the whole
-                    // row; a row with heads finds each element's base -- S before the last head
-                    // at or before it
+                    // of the 1-D stream kernel give S; a row without heads (a bit of the head
+                    // warp's row mask: most rows unless segments are short) subtracts one base B
+                    // for the whole row; a row with heads finds each element's base -- S before
+                    // the last head at or before it.  Whole portions (all but the array's two
+                    // ends) run a copy of the loop without any bounds logic.
                     if (warp == 0 && lane == 0 && ch == warp) SEG_TRACE(r, 6);
                     SEG_WAIT(&pre[b], par(r));  // the chunk's S and B (the ledger)
-                    A base = chunk_pre[b * MAXC + ch], bin = chunk_B[b * MAXC + ch];
-                    const int one = a.one;
+                    auto sub_rows = [&](auto whole_c) {
+                        constexpr bool W = decltype(whole_c)::value;
+                        A base = chunk_pre[b * MAXC + ch], bin = chunk_B[b * MAXC + ch];
+                        const int one = a.one;
+                        const uint32_t rh = PS_SEG_EXP == 12 ? 0u : row_heads[b] >> (ch * ROWS);
+                        auto put = [&](int64_t q0, const TOut (&y)[VEC]) {
+                            if constexpr (W) {
+                                if (PS_SEG_EXP == 13 && a.exclusive != 77) return;  // ablation: no output stores
+                                constexpr int NV = VEC * sizeof(TOut) / 32;
+#pragma unroll
+                                for (int k = 0; k < NV; ++k)
+                                    stg256_policy(out + p0 + q0 + k * (32 / sizeof(TOut)),
+                                                  pack<TOut>(&y[k * (32 / sizeof(TOut))]), pol);
+                            } else {
+                                store_row(q0, y);
+                            }
+                        };
 #pragma unroll SEG_UNROLL
-                    for (int rr = 0; rr < ROWS; ++rr) {
-                        const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
-                        TIn x[VEC];
-                        if (w) {
-                            unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < VEC; ++j) {
-                                const int64_t pos = p0 + q0 + j;
-                                x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
-                            }
-                        }
-                        const uint32_t hbr = heads_at(bm, q0);
-                        A p[VEC];  // in-lane inclusive prefix
-                        p[0] = (A)x[0];
-#pragma unroll
-                        for (int j = 1; j < VEC; ++j) p[j] = add_widen(p[j - 1], x[j], one);
-                        const uint32_t bh = PS_SEG_EXP == 12 ? 0u : __ballot_sync(FULL, hbr != 0u);
-                        const A sc = PS_SEG_EXP == 14 ? p[VEC - 1] * (lane + 1) : warp_scan_pred(p[VEC - 1]);  // 14: ablation
-                        const A exs = sc - p[VEC - 1], rts = PS_SEG_EXP == 14 ? sc + lane : shfl_idx(sc, 31);
-                        TOut y[VEC];
-                        if (bh == 0u) {
-                            const A d = base + exs - bin;  // the open segment's sum before this lane
-                            if (a.exclusive) {
-                                y[0] = (TOut)d;
-#pragma unroll
-                                for (int j = 1; j < VEC; ++j) y[j] = (TOut)(d + p[j - 1]);
+                        for (int rr = 0; rr < ROWS; ++rr) {
+                            const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
+                            TIn x[VEC];
+                            if constexpr (W) {
+                                unpack<TIn>(lds256<(sizeof(TIn) == 8)>(sb + q0), x);
                             } else {
 #pragma unroll
-                                for (int j = 0; j < VEC; ++j) y[j] = (TOut)(d + p[j]);
-                            }
-                            store_row(q0, y);
-                            if constexpr (EMIT)
-                                if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = d + p[VEC - 1];
-                        } else {
-                            // o[j]: the sum since the lane's last head at or before j (since the
-                            // lane's start before its first head); pb: the lane's sum before its last head
-                            A pb = (A)0, o[VEC];
-                            o[0] = p[0];
-#pragma unroll
-                            for (int j = 1; j < VEC; ++j) {
-                                if ((hbr >> j) & 1u) pb = p[j - 1];
-                                o[j] = p[j] - pb;
-                            }
-                            const A hrel = exs + pb;  // row-relative S before this lane's last head
-                            const uint32_t below = bh & ((1u << lane) - 1u);
-                            const A hsrc = shfl_idx(hrel, below ? 31 - __clz((int)below) : lane);
-                            const A Bl = below ? base + hsrc : bin;
-                            const A d = base + exs - Bl;
-                            A inc[VEC];
-                            uint32_t seen = 0;
-#pragma unroll
-                            for (int j = 0; j < VEC; ++j) {
-                                seen |= (hbr >> j) & 1u;
-                                inc[j] = seen ? o[j] : d + p[j];
-                            }
-                            if (a.exclusive) {
-#pragma unroll
-                                for (int j = 0; j < VEC; ++j)
-                                    y[j] = ((hbr >> j) & 1u) ? (TOut)0 : (TOut)(j == 0 ? d : inc[j - 1]);
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
-                            }
-                            store_row(q0, y);
-                            if constexpr (EMIT) {
-                                if (tot) {
-                                    emit_totals(q0, hbr, inc, d);
-                                    if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                                for (int j = 0; j < VEC; ++j) {
+                                    const int64_t pos = p0 + q0 + j;
+                                    x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
                                 }
                             }
-                            bin = base + shfl_idx(hrel, 31 - __clz((int)bh));
+                            A p[VEC];  // in-lane inclusive prefix
+                            p[0] = (A)x[0];
+#pragma unroll
+                            for (int j = 1; j < VEC; ++j) p[j] = add_widen(p[j - 1], x[j], one);
+                            const A sc = PS_SEG_EXP == 14 ? p[VEC - 1] * (lane + 1) : warp_scan_pred(p[VEC - 1]);  // 14: ablation
+                            const A exs = sc - p[VEC - 1], rts = PS_SEG_EXP == 14 ? sc + lane : shfl_idx(sc, 31);
+                            TOut y[VEC];
+                            if (!((rh >> rr) & 1u)) {
+                                const A d = base + exs - bin;  // the open segment's sum before this lane
+                                if (a.exclusive) {
+                                    y[0] = (TOut)d;
+#pragma unroll
+                                    for (int j = 1; j < VEC; ++j) y[j] = (TOut)(d + p[j - 1]);
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < VEC; ++j) y[j] = (TOut)(d + p[j]);
+                                }
+                                put(q0, y);
+                                if constexpr (EMIT)
+                                    if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = d + p[VEC - 1];
+                            } else {
+                                const uint32_t hbr = heads_at(bm, q0);
+                                const uint32_t bh = __ballot_sync(FULL, hbr != 0u);
+                                // o[j]: the sum since the lane's last head at or before j (since the
+                                // lane's start before its first head); pb: the lane's sum before its last head
+                                A pb = (A)0, o[VEC];
+                                o[0] = p[0];
+#pragma unroll
+                                for (int j = 1; j < VEC; ++j) {
+                                    if ((hbr >> j) & 1u) pb = p[j - 1];
+                                    o[j] = p[j] - pb;
+                                }
+                                const A hrel = exs + pb;  // row-relative S before this lane's last head
+                                const uint32_t below = bh & ((1u << lane) - 1u);
+                                const A hsrc = shfl_idx(hrel, below ? 31 - __clz((int)below) : lane);
+                                const A Bl = below ? base + hsrc : bin;
+                                const A d = base + exs - Bl;
+                                A inc[VEC];
+                                uint32_t seen = 0;
+#pragma unroll
+                                for (int j = 0; j < VEC; ++j) {
+                                    seen |= (hbr >> j) & 1u;
+                                    inc[j] = seen ? o[j] : d + p[j];
+                                }
+                                if (a.exclusive) {
+#pragma unroll
+                                    for (int j = 0; j < VEC; ++j)
+                                        y[j] = ((hbr >> j) & 1u) ? (TOut)0 : (TOut)(j == 0 ? d : inc[j - 1]);
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
+                                }
+                                put(q0, y);
+                                if constexpr (EMIT) {
+                                    if (tot) {
+                                        emit_totals(q0, hbr, inc, d);
+                                        if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                                    }
+                                }
+                                bin = base + shfl_idx(hrel, 31 - __clz((int)bh));
+                            }
+                            base += rts;
                         }
-                        base += rts;
-                    }
+                    };
+#if PS_SEG_WSPLIT
+                    if (w) sub_rows(std::true_type{});
+                    else sub_rows(std::false_type{});
+#else
+                    sub_rows(std::false_type{});
+#endif
                     continue;
                 }
                 A v[ROWS][VEC];
