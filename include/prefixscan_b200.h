@@ -14,7 +14,7 @@
  *                         simd.py:104-121 _make_simd_accumulate_kernel
  *   ps_add_offset      <- core.py:103-106 _increment_kernel    (+ core.py:135-138 sequential_increment)
  *   ps_scan_batched    <- simd.py:164-206 vertical pass kernels (row seeds in, row totals out)
- *   ps_scan_segmented  <- (no reference kernel; CSR-segment form of the same look-back scan)
+ *   ps_scan_segmented  <- (no reference kernel; CSR-segment form of the per-chunk scans of simd.py:164-206)
  *   ps_scan_host       <- engine.py:219-248 ScanEngine.run on host buffers (end-to-end call:
  *                         host->device copy, scan, device->host copy, pipelined)
  *
@@ -124,7 +124,12 @@ size_t ps_scan_segmented_scratch_bytes(int64_t n, int dtype_in, int dtype_out);
  * in[seg_offsets[s] .. seg_offsets[s+1]), seg_offsets (device int64, nseg+1
  * entries, non-decreasing, seg_offsets[0] == 0, seg_offsets[nseg] == n).
  * Every segment restarts at zero; seg_totals (device acc-typed, nullable)
- * receives each segment's sum. */
+ * receives each segment's sum (0 for an empty segment).  Large inputs run on
+ * the shared-memory-region kernel (seg_stream.cuh: head bitmap pre-pass, one
+ * HBM read and one write per element); for integer scans with 64-bit outputs
+ * the totals are read back from `out` by a small kernel after the scan (the
+ * inclusive value of a segment's last element), otherwise the scanners emit
+ * them.  seg_totals must not overlap in / out. */
 int ps_scan_segmented(const void *in, void *out, int64_t n, const int64_t *seg_offsets,
                       int64_t nseg, int dtype_in, int dtype_out, int exclusive, void *seg_totals,
                       void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream);
@@ -292,6 +297,9 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *                      rounds and rows kernels sleeps with probability
  *                      stall_prob/1024 for a hashed time in [0, stall_ns)
  *                      (stall_ns 0 = off; the reference's delay_hook, engine.py:91)
+ *   "seg_kernel"       ps_scan_segmented: 0 = auto (shared-memory regions from
+ *                      rounds_min_bytes of input, look-back tiles below), 1 = look-back
+ *                      tiles, 2 = shared-memory regions
  *   "float_exact"      stream kernel, float32 -> float32: 0 = in-chunk scans in float32
  *                      with the float64 carry applied as a float pair (FP32 pipe only,
  *                      <= 1e-6 relative to float32(cumsum(float64))), 1 = float64 per

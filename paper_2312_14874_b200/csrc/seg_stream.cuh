@@ -227,6 +227,18 @@ template <typename A> __device__ __forceinline__ A warp_scan_pred(A v) {
     return v;
 }
 
+// the two 16-byte descriptors of one portion of an integer scan (total; sum before the last
+// head + head flag) sit side by side and are polled with ONE 256-bit strong load -- each
+// half carries its own tag, so tearing between the halves is harmless.  Five loads per lane
+// and region (as the 1-D kernel) instead of ten: the next region's gather can be in flight
+// during the fold without its loads holding the scoreboards the fold's shuffles wait on.
+__device__ __forceinline__ void ld_desc_pair(const ulonglong2 *p, ulonglong2 &a, ulonglong2 &b) {
+    asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y)
+                 : "l"(p)
+                 : "memory");
+}
+
 template <typename A> struct SegPair {
     A v;
     uint32_t f;
@@ -480,7 +492,6 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
         const int rw = warp - SW;
         if constexpr (SUB) {
             // per chunk: plain sum, and the sum of the elements before its last head
-            ulonglong2 *desc2 = a.desc + a.rounds * G;
             for (int64_t r = 0; r < a.rounds; ++r) {
                 const int b = (int)(r % NBUF);
                 SEG_WAIT(&full[b], par(r));
@@ -607,8 +618,9 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                     const A before = warp_sum(lane < kl ? ct : (A)0);
                     const A plh = before + (kl >= 0 ? chunk_plh[b * MAXC + kl] : (A)0);
                     if (lane == 0) {
-                        st_desc(desc2 + r * G + c, want | ST_A | (fb ? SEG_FLAG : 0ull), acc_to_bits<A>(plh));
-                        st_desc(a.desc + r * G + c, want | ST_A, acc_to_bits<A>(t));
+                        ulonglong2 *rec = a.desc + 2 * (r * G + c);  // {total, sum before the last head}
+                        st_desc(rec + 1, want | ST_A | (fb ? SEG_FLAG : 0ull), acc_to_bits<A>(plh));
+                        st_desc(rec, want | ST_A, acc_to_bits<A>(t));
                         SEG_TRACE(r, 2);
                         mbar_arrive(&red[b]);
                     }
@@ -686,17 +698,13 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
             // took four masked sums with butterfly reductions plus per-group shuffles: ~300
             // dependent instructions, 1.3-1.5 us per region -- the kernel's critical loop.)
             constexpr int LP = GATHER_LP;
-            ulonglong2 *desc2 = a.desc + a.rounds * G;
             A carry = (A)0, bcarry = (A)0;
             ulonglong2 dn[LP], dh[LP];
             auto issue = [&](int64_t r) {
 #pragma unroll
                 for (int i = 0; i < LP; ++i) {
                     const int j = lane + 32 * i;  // coalesced polls; transposed through shared memory below
-                    if (j < G) {
-                        dn[i] = ld_desc(a.desc + r * G + j);
-                        dh[i] = ld_desc(desc2 + r * G + j);
-                    }
+                    if (j < G) ld_desc_pair(a.desc + 2 * (r * G + j), dn[i], dh[i]);
                 }
             };
             issue(0);
@@ -735,10 +743,7 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                         __nanosleep(PS_SEG_POLL_NS);
 #pragma unroll
                         for (int i = 0; i < LP; ++i)
-                            if ((pending >> i) & 1) {
-                                dn[i] = ld_desc(a.desc + r * G + lane + 32 * i);
-                                dh[i] = ld_desc(desc2 + r * G + lane + 32 * i);
-                            }
+                            if ((pending >> i) & 1) ld_desc_pair(a.desc + 2 * (r * G + lane + 32 * i), dn[i], dh[i]);
                     }
                 }
                 if (lane == 0) SEG_TRACE(r, 4);
