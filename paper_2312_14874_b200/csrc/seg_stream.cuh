@@ -638,11 +638,20 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
             const int64_t p0 = p0_of(r);
             const bool w = whole(r);
             const bool lv = w || live(r);
+            if (lv) SEG_WAIT(&hdr[b], par(r));  // the chunks' last heads (head warp)
             for (int64_t ch = rw; ch < NCHUNK; ch += RWP) {
-                Pair agg{(A)0, 0u};
+                // the chunk's aggregate under the segmented-sum operator: (any head, sum of the
+                // elements from its last head on -- of all of them if it holds none).  The head
+                // warp found the last head, so this is one masked sum: lanes, then one warp tree
+                // (a fixed order: deterministic)
+                A acc = (A)0;
+                int lh = -1;
                 if (lv) {
-#pragma unroll
-                    for (int rr = 0; rr < ROWS; ++rr) {
+                    lh = chunk_lh[b * MAXC + ch];
+                    const int lrow = lh >= 0 ? lh / ROW_ELEMS : -1;
+                    const int lim = lh - lrow * ROW_ELEMS - lane * VEC;  // row lrow: this lane's elements j >= lim count
+#pragma unroll 1
+                    for (int rr = lrow > 0 ? lrow : 0; rr < ROWS; ++rr) {
                         const int64_t q0 = ch * CHUNK + rr * ROW_ELEMS + lane * VEC;
                         TIn x[VEC];
                         if (w) {
@@ -654,22 +663,25 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                                 x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
                             }
                         }
-                        const uint32_t hb = heads_at(bm, q0);
-                        Pair lp{(A)0, hb != 0u};
+                        if (rr == lrow) {
 #pragma unroll
-                        for (int j = 0; j < VEC; ++j) lp.v = ((hb >> j) & 1u) ? (A)x[j] : lp.v + (A)x[j];
-                        // ordered reduction over the lanes of the row: lane 0 ends with it
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const Pair y{shfl_down(lp.v, d), __shfl_down_sync(FULL, lp.f, d)};
-                            if ((lane & (2 * d - 1)) == 0) lp = seg_combine(lp, y);
+                            for (int j = 0; j < VEC; ++j)
+                                if (j < lim) x[j] = (TIn)0;
                         }
-                        agg = seg_combine(agg, lp);  // meaningful on lane 0
+                        A v[VEC];
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) v[j] = (A)x[j];
+#pragma unroll
+                        for (int d = 1; d < VEC; d <<= 1)
+#pragma unroll
+                            for (int j = 0; j + d < VEC; j += 2 * d) v[j] += v[j + d];
+                        acc += v[0];
                     }
+                    acc = warp_sum(acc);
                 }
                 if (lane == 0) {
-                    chunk_tot[b * MAXC + ch] = agg.v;
-                    chunk_f[b * MAXC + ch] = agg.f;
+                    chunk_tot[b * MAXC + ch] = acc;
+                    chunk_f[b * MAXC + ch] = lh >= 0;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1057,9 +1069,16 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
 #endif
                     continue;
                 }
-                A v[ROWS][VEC];
-                Pair ex[ROWS], rt[ROWS];
-#pragma unroll
+                // floats: one row at a time (rolled: the hot loops of all roles have to fit the
+                // instruction cache -- the unrolled form of this loop thrashed it, 1.7 stall
+                // cycles per issue waiting for instructions).  A row without heads is the plain
+                // scan of the 1-D kernel on top of the open segment's running sum; a row with
+                // heads runs the (flag, value) pair operator
+                if (warp == 0 && lane == 0 && ch == warp) SEG_TRACE(r, 6);
+                SEG_WAIT(&pre[b], par(r));  // the chunk carries of region r (the ledger)
+                A base = chunk_pre[b * MAXC + ch];
+                const uint32_t rh = row_heads[b] >> (ch * ROWS);
+#pragma unroll 1
                 for (int rr = 0; rr < ROWS; ++rr) {
                     const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
                     TIn x[VEC];
@@ -1072,45 +1091,66 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                             x[j] = (pos >= a.lo && pos < a.hi) ? in[pos] : (TIn)0;
                         }
                     }
-                    hb[rr] = heads_at(bm, q0);
-                    // in-lane segmented prefix: v[j] = sum since the last head at or before j
-                    // (or since the lane's first element if there is none)
-                    A run = (A)0;
-#pragma unroll
-                    for (int j = 0; j < VEC; ++j) {
-                        run = ((hb[rr] >> j) & 1u) ? (A)x[j] : run + (A)x[j];
-                        v[rr][j] = run;
-                    }
-                    const Pair inc = seg_warp_scan(Pair{run, hb[rr] != 0u}, lane);
-                    ex[rr] = seg_shfl_up(inc, 1);
-                    if (lane == 0) ex[rr] = Pair{(A)0, 0u};
-                    rt[rr] = Pair{shfl_idx(inc.v, 31), __shfl_sync(FULL, inc.f, 31)};
-                }
-                if (warp == 0 && lane == 0 && ch == 0) SEG_TRACE(r, 6);
-                SEG_WAIT(&pre[b], par(r));  // the chunk carries of region r (the ledger)
-                A base = chunk_pre[b * MAXC + ch];
-#pragma unroll
-                for (int rr = 0; rr < ROWS; ++rr) {
-                    const int64_t q0 = c0 + rr * ROW_ELEMS + lane * VEC;
-                    const A lane_in = ex[rr].f ? ex[rr].v : base + ex[rr].v;  // sum before the lane's first element
-                    A inc[VEC];
-                    uint32_t seen = 0;
-#pragma unroll
-                    for (int j = 0; j < VEC; ++j) {
-                        seen |= (hb[rr] >> j) & 1u;
-                        inc[j] = seen ? v[rr][j] : lane_in + v[rr][j];
-                    }
+                    A v[VEC], inc[VEC];
                     TOut y[VEC];
-                    if (a.exclusive) {
+                    if (!((rh >> rr) & 1u)) {
+                        v[0] = (A)x[0];
 #pragma unroll
-                        for (int j = 0; j < VEC; ++j)
-                            y[j] = ((hb[rr] >> j) & 1u) ? (TOut)0 : (TOut)(j == 0 ? lane_in : inc[j - 1]);
+                        for (int j = 1; j < VEC; ++j) v[j] = v[j - 1] + (A)x[j];
+                        A sc = v[VEC - 1];
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const A t = shfl_up(sc, d);
+                            if (lane >= d) sc += t;
+                        }
+                        A exs = shfl_up(sc, 1);
+                        if (lane == 0) exs = (A)0;
+                        const A lane_in = base + exs;
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) inc[j] = lane_in + v[j];
+                        if (a.exclusive) {
+                            y[0] = (TOut)lane_in;
+#pragma unroll
+                            for (int j = 1; j < VEC; ++j) y[j] = (TOut)inc[j - 1];
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
+                        }
+                        store_row(q0, y);
+                        if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                        base += shfl_idx(sc, 31);
                     } else {
+                        const uint32_t hbr = heads_at(bm, q0);
+                        // in-lane segmented prefix: v[j] = sum since the last head at or before j
+                        // (or since the lane's first element if there is none)
+                        A run = (A)0;
 #pragma unroll
-                        for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
+                        for (int j = 0; j < VEC; ++j) {
+                            run = ((hbr >> j) & 1u) ? (A)x[j] : run + (A)x[j];
+                            v[j] = run;
+                        }
+                        const Pair pinc = seg_warp_scan(Pair{run, hbr != 0u}, lane);
+                        Pair ex = seg_shfl_up(pinc, 1);
+                        if (lane == 0) ex = Pair{(A)0, 0u};
+                        const Pair rt{shfl_idx(pinc.v, 31), __shfl_sync(FULL, pinc.f, 31)};
+                        const A lane_in = ex.f ? ex.v : base + ex.v;  // sum before the lane's first element
+                        uint32_t seen = 0;
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            seen |= (hbr >> j) & 1u;
+                            inc[j] = seen ? v[j] : lane_in + v[j];
+                        }
+                        if (a.exclusive) {
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j)
+                                y[j] = ((hbr >> j) & 1u) ? (TOut)0 : (TOut)(j == 0 ? lane_in : inc[j - 1]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
+                        }
+                        emit(q0, hbr, inc, y, lane_in);
+                        base = rt.f ? rt.v : base + rt.v;
                     }
-                    emit(q0, hb[rr], inc, y, lane_in);
-                    base = rt[rr].f ? rt[rr].v : base + rt[rr].v;
                 }
             }
         }
