@@ -91,20 +91,42 @@ while time.time() < deadline:
         if excl:
             want = want - b
         compare(o.cpu().numpy(), want, f"rows {rows}x{cols} excl={excl} {knobs} seeded={seeded}")
-    if cases % 13 == 0:  # CSR segmented
-        m = int(rng.choice([1000, 1 << 20, 3_000_001]))
-        nseg = int(rng.choice([1, 10, 1000, m // 4 + 1]))
-        cuts = np.sort(rng.integers(0, m + 1, nseg - 1))
+    if cases % 5 == 0:  # CSR segmented: both kernels, dtype pairs, totals, in place, unaligned views
+        m = int(rng.choice([1000, 1 << 20, 3_000_001, 9_000_013]))
+        nseg = int(rng.choice([1, 10, 1000, m // 300 + 1, m // 4 + 1]))
+        cuts = np.sort(rng.integers(0, m + 1, nseg - 1))  # repeated offsets = empty segments
         offs = np.concatenate([[0], cuts, [m]]).astype(np.int64)
-        v = rng.integers(0, 100, m).astype(np.int32)
-        o = torch.empty(m, dtype=torch.int64, device="cuda")
-        dev.scan_segmented(torch.from_numpy(v).cuda(), torch.from_numpy(offs).cuda(), o, exclusive=excl)
-        c = np.cumsum(v.astype(np.int64))
-        starts = np.repeat(offs[:-1], np.diff(offs))
-        want = c - np.where(starts > 0, c[np.maximum(starts - 1, 0)], 0)
-        if excl:
-            want = want - v
-        compare(o.cpu().numpy(), want, f"segmented m={m} nseg={nseg} excl={excl}")
+        sdin, sdout = PAIRS[int(rng.integers(0, len(PAIRS)))]
+        fl = np.dtype(sdout).kind == "f"
+        acc = np.float64 if fl else (np.uint64 if np.dtype(sdin).kind == "u" else np.int64)
+        # floats on a 2^-10 grid: every float64 partial sum is exact, so the cumsum-difference
+        # reference below has no cancellation error and the comparison is meaningful
+        v = (rng.integers(0, 1024, m) / 1024.0).astype(sdin) if np.dtype(sdin).kind == "f" else rng.integers(0, 100, m).astype(sdin)
+        sk = int(rng.integers(0, 3))
+        lib.ps_set_tuning(b"seg_kernel", sk)
+        lead = int(rng.integers(0, 4))
+        xin = torch.empty(m + lead, dtype=getattr(torch, np.dtype(sdin).name), device="cuda")[lead:]
+        xin.copy_(torch.from_numpy(v))
+        inplace = sdin == sdout and rng.random() < 0.3
+        o = xin if inplace else torch.empty(m + lead, dtype=getattr(torch, np.dtype(sdout).name), device="cuda")[lead:]
+        tots = torch.empty(nseg, dtype=getattr(torch, np.dtype(acc).name), device="cuda") if rng.random() < 0.7 else None
+        dev.scan_segmented(xin, torch.from_numpy(offs).cuda(), o, exclusive=excl, seg_totals=tots)
+        lib.ps_set_tuning(b"seg_kernel", 0)
+        c = np.concatenate([[acc(0)], np.cumsum(v.astype(acc))]).astype(acc)
+        seg_of = np.searchsorted(offs, np.arange(m), side="right") - 1
+        want = ((c[:-1] if excl else c[1:]) - c[offs[seg_of]]).astype(sdout)
+        what = f"segmented {np.dtype(sdin).name}->{np.dtype(sdout).name} m={m} nseg={nseg} excl={excl} kernel={sk} lead={lead} inplace={inplace}"
+        compare(o.cpu().numpy(), want, what)
+        if tots is not None:
+            wt = (c[offs[1:]] - c[offs[:-1]]).astype(acc)
+            gt = tots.cpu().numpy()
+            if fl:
+                ok = np.allclose(gt, wt, rtol=1e-9, atol=1e-6)
+            else:
+                ok = np.array_equal(gt, wt)
+            if not ok:
+                print("MISMATCH totals", what, flush=True)
+                sys.exit(1)
     if cases % 11 == 0:  # compaction
         m = int(rng.choice([1000, 1 << 20, 5_000_000]))
         v = rng.integers(-1000, 1000, m).astype(np.int32)
