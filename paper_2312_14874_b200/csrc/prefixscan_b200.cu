@@ -435,7 +435,7 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     const size_t clear = L.total - L.off_dup;  // repeat flags + bitmap
     cudaError_t e = cudaMemsetAsync(dup, 0, clear, s);
     if (e != cudaSuccess) return cuda_rc(e);
-    const int64_t threads = (L.Q + 1 > nseg + 1 ? L.Q + 1 : nseg + 1);
+    const int64_t threads = nseg + 1;  // one per offset
     seg_prepare_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(offsets, nseg, n, lead, P, L.Q, lb, dup, bm);
     void *params[] = {&a};
 #ifdef PS_SEG_TRACE
