@@ -418,7 +418,7 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     a.dupflag = dup;
     a.bitmap = bm;
     using A = typename AccOf<TIn>::type;
-    constexpr bool GATHER = (A)0.5 == (A)0 && sizeof(TOut) == 8;  // totals read back from the output
+    constexpr bool GATHER = sizeof(TOut) == 8;  // accumulator-typed output: totals read back from it
     a.totals = GATHER ? nullptr : totals;
     if (!GATHER && totals) {  // emitted by the scanners: empty segments keep the zero
         cudaError_t ze = cudaMemsetAsync(totals, 0, (size_t)nseg * 8, s);

@@ -138,11 +138,13 @@ __global__ void seg_prepare_kernel(const int64_t *off, int64_t nseg, int64_t n, 
         for (int64_t q = qhi + 1; q <= Q; ++q) lb[q] = (nseg + 1) << 2;
 }
 
-// Segment totals of the integer instantiations with 64-bit outputs are read back from the
-// scan's own output after the launch (the inclusive value of a segment's last element is its
-// total, exact in two's complement) instead of being scattered by the scanners: one 32-byte
-// sector per segment against a per-head loop on the scanners' serial path.  An exclusive scan
-// keeps the last element in totals[] from before the launch (input and output may alias).
+// Segment totals of the instantiations with 8-byte (= accumulator-typed) outputs are read back
+// from the scan's own output after the launch (the inclusive value of a segment's last
+// element is its total: exact in two's complement for integers, the very float64 value the
+// scanners would have stored for floats) instead of being scattered by the scanners: one
+// 64-byte fetch per segment against a per-head loop on the scanners' serial path.  An
+// exclusive scan keeps the last element in totals[] from before the launch (input and output
+// may alias) and adds it to the last exclusive value.
 template <typename TIn, typename A>
 __global__ void seg_last_in_kernel(const TIn *in, const int64_t *off, int64_t nseg, A *tot) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -162,7 +164,7 @@ __global__ void seg_totals_gather_kernel(const TOut *out, const int64_t *off, in
         if constexpr (sizeof(TOut) == 8) {
             uint64_t raw;
             asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(raw) : "l"(out + e - 1));
-            v = (A)(TOut)raw;
+            v = (A) * reinterpret_cast<const TOut *>(&raw);
         } else {
             v = (A)out[e - 1];  // (instantiated, never launched: narrow outputs emit their totals in-kernel)
         }
@@ -282,8 +284,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
     // sum and B = S before the last head at or before the element (exact in two's
     // complement); floats: the (flag, value) pair operator (no cancellation)
     constexpr bool SUB = (A)0.5 == (A)0;
-    // integer scans with 64-bit outputs: totals are gathered after the launch (seg_totals_gather_kernel)
-    constexpr bool EMIT = !(SUB && sizeof(TOut) == 8);
+    // scans with 64-bit outputs: totals are gathered after the launch (seg_totals_gather_kernel)
+    constexpr bool EMIT = sizeof(TOut) != 8;  // 8-byte outputs are accumulator-typed: totals gathered from them
     static_assert(32 % VEC == 0, "a lane's head bits sit in one bitmap word");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -931,9 +933,11 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
             const bool tail_tot = tot && p0 + P == a.hi && m.next_head;
             auto emit = [&](int64_t q0, uint32_t hbits, const A (&inc)[VEC], const TOut (&y)[VEC], A lane_prev) {
                 store_row(q0, y);
-                if (!tot) return;
-                emit_totals(q0, hbits, inc, lane_prev);
-                if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                if constexpr (EMIT) {
+                    if (!tot) return;
+                    emit_totals(q0, hbits, inc, lane_prev);
+                    if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                }
             };
             for (int64_t ch = warp; ch < NCHUNK; ch += SW) {
                 const int64_t c0 = ch * CHUNK;
@@ -1098,7 +1102,8 @@ __global__ void __launch_bounds__((SW + RWP + 3) * 32, 1) seg_stream_kernel(cons
                             for (int j = 0; j < VEC; ++j) y[j] = (TOut)inc[j];
                         }
                         store_row(q0, y);
-                        if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
+                        if constexpr (EMIT)
+                            if (tail_tot && q0 + VEC == P) tot[m.lb1 - 1] = inc[VEC - 1];
                         base += shfl_idx(sc, 31);
                     } else {
                         const uint32_t hbr = heads_at(bm, q0);
