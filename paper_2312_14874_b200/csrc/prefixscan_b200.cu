@@ -388,7 +388,8 @@ size_t seg_stream_scratch_bytes(int64_t n, int elem_bytes) {
 // returns -1 when the buffers do not suit the region kernel (caller falls back)
 template <typename TIn, typename TOut>
 int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offsets, int64_t nseg, int exclusive,
-                      void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s) {
+                      void *totals, void *scratch, size_t scratch_bytes, uint32_t epoch, cudaStream_t s,
+                      int64_t ucols = 0) {  // offsets == nullptr: nseg uniform segments of ucols elements
     const uintptr_t ain = (uintptr_t)in % 32;
     const int64_t lead = (ain % sizeof(TIn)) ? -1 : (int64_t)(ain / sizeof(TIn));
     const bool vec = lead >= 0 && ((uintptr_t)out % 32) == (uintptr_t)((lead * sizeof(TOut)) % 32) &&
@@ -426,7 +427,7 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     }
     if (GATHER && totals && exclusive)
         seg_last_in_kernel<TIn, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
-            static_cast<const TIn *>(in), offsets, nseg, static_cast<A *>(totals));
+            static_cast<const TIn *>(in), offsets, ucols, nseg, static_cast<A *>(totals));
     a.desc = reinterpret_cast<ulonglong2 *>(sc + 256);
     a.epoch = epoch;
     a.exclusive = exclusive;
@@ -436,7 +437,8 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     cudaError_t e = cudaMemsetAsync(dup, 0, clear, s);
     if (e != cudaSuccess) return cuda_rc(e);
     const int64_t threads = nseg + 1;  // one per offset
-    seg_prepare_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(offsets, nseg, n, lead, P, L.Q, lb, dup, bm);
+    seg_prepare_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(offsets, ucols, nseg, n, lead, P, L.Q, lb, dup,
+                                                                          bm);
     void *params[] = {&a};
 #ifdef PS_SEG_TRACE
     static uint64_t *trace = nullptr;
@@ -469,12 +471,12 @@ int launch_seg_stream(const void *in, void *out, int64_t n, const int64_t *offse
     if (GATHER && PS_SEG_INCLEAR) {  // these instantiations cleared the repeat flags and the bitmap as they consumed them
         if (totals)
             seg_totals_gather_kernel<TOut, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
-                static_cast<const TOut *>(out), offsets, nseg, static_cast<A *>(totals), exclusive);
+                static_cast<const TOut *>(out), offsets, ucols, nseg, static_cast<A *>(totals), exclusive);
         return launch_rc();
     }
     if (GATHER && totals)
         seg_totals_gather_kernel<TOut, A><<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(
-            static_cast<const TOut *>(out), offsets, nseg, static_cast<A *>(totals), exclusive);
+            static_cast<const TOut *>(out), offsets, ucols, nseg, static_cast<A *>(totals), exclusive);
     return cuda_rc(cudaMemsetAsync(dup, 0, clear, s));
 }
 
@@ -613,9 +615,18 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     // many short contiguous rows without seeds: one flat segmented scan with uniform
     // segments (a look-back tile per row would leave most of each tile idle)
     if (rows > 1 && g_tune.tiles_row_lead && !seed_terms && seed_bits == 0 && !mail && ld_in == cols && ld_out == cols &&
-        cols * 4 <= TILE && scratch && scratch_bytes >= seg_scratch_bytes(rows * cols, (int)sizeof(TIn)))
+        cols * 4 <= TILE && scratch && scratch_bytes >= seg_scratch_bytes(rows * cols, (int)sizeof(TIn))) {
+        // large inputs: the shared-memory-region kernel with computed offsets (one HBM read and
+        // write per element; 2^20 rows x 250 int32 -> int64: 0.31 -> ~0.8 of the peak)
+        if (g_tune.seg_kernel != 1 && rows * cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes &&
+            scratch_bytes >= seg_stream_scratch_bytes(rows * cols, (int)sizeof(TIn))) {
+            const int rc = launch_seg_stream<TIn, TOut>(in, out, rows * cols, nullptr, rows, exclusive, totals, scratch,
+                                                        scratch_bytes, epoch, s, cols);
+            if (rc >= 0) return rc;
+        }
         return launch_segmented<TIn, TOut>(in, out, rows * cols, nullptr, rows, exclusive, totals, scratch, epoch, s,
                                            cols);
+    }
     a.tiles_per_row = (a.lead + max_lead + cols + TILE - 1) / TILE;
     const int64_t tiles = rows * a.tiles_per_row;
     if (tiles > 0x7fffffffLL) return PS_ERR_ARG;
@@ -922,7 +933,13 @@ int ps_scan(const void *in, void *out, int64_t n, int dtype_in, int dtype_out, i
 size_t ps_scan_batched_scratch_bytes(int64_t rows, int64_t cols, int dtype_in, int dtype_out) {
     if (!pair_ok(dtype_in, dtype_out) || rows < 0 || cols < 0) return 0;
     const int64_t tile = tile_of_dtype(dtype_in);
-    return desc_bytes(rows * ((cols + tile - 1) / tile + 1));
+    size_t need = desc_bytes(rows * ((cols + tile - 1) / tile + 1));
+    if (rows > 1 && cols * 4 <= tile) {  // short rows may run as one segmented scan of the flat array
+        const size_t a = seg_scratch_bytes(rows * cols, (int)dsize(dtype_in));
+        const size_t b = seg_stream_scratch_bytes(rows * cols, (int)dsize(dtype_in));
+        need = std::max(need, std::max(a, b));
+    }
+    return need;
 }
 
 int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
@@ -937,8 +954,19 @@ int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64
     if (!in || !out) return PS_ERR_ARG;
     if (in == out && (dsize(dtype_in) != dsize(dtype_out) || ld_in != ld_out)) return PS_ERR_OVERLAP;
     if (rows == 1) ld_in = ld_out = cols;
+    // short contiguous rows of a large batch run as one segmented scan of the flat array on the
+    // shared-memory-region kernel (launch_scan's uniform-segment route): a row per TMA item
+    // leaves the rows kernel at 0.05-0.4 of the peak below ~2 KiB per row, the region kernel
+    // holds 0.6-0.8 (scripts/short_rows_cross.py; crossover 2 KiB rows for integers, 1 KiB floats)
+    const int64_t row_bytes = cols * (int64_t)dsize(dtype_in);
+    const bool floats = dtype_in == PS_DTYPE_FLOAT32 || dtype_in == PS_DTYPE_FLOAT64;
+    const bool flat_segments = rows > 1 && !row_seeds && ld_in == cols && ld_out == cols && g_tune.rows_kernel != 2 &&
+                               g_tune.seg_kernel != 1 && g_tune.tiles_row_lead && row_bytes <= (floats ? 1024 : 2048) &&
+                               rows * row_bytes >= g_tune.rounds_min_bytes && scratch &&
+                               scratch_bytes >= seg_stream_scratch_bytes(rows * cols, (int)dsize(dtype_in)) &&
+                               scratch_bytes >= seg_scratch_bytes(rows * cols, (int)dsize(dtype_in));
 #define CALL(TI, TO)                                                                                            \
-    if (rows > 1 && rows_kernel_applies<TI, TO>(in, rows, cols, ld_in))                                         \
+    if (rows > 1 && !flat_segments && rows_kernel_applies<TI, TO>(in, rows, cols, ld_in))                       \
         return launch_rows<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, row_seeds, row_totals, scratch, \
                                    scratch_bytes, s);                                                           \
     return launch_scan<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, 0, row_seeds, row_seeds ? rows : 0, \

@@ -109,6 +109,12 @@ struct SegStreamArgs {
     int one;  // 1 (the opaque multiplier of add_widen)
 };
 
+// offsets of uniform segments (rows of `ucols` elements, ps_scan_batched's short rows) are
+// computed, not read
+__device__ __forceinline__ int64_t seg_off(const int64_t *off, int64_t ucols, int64_t t) {
+    return off ? __ldg(off + t) : t * ucols;
+}
+
 // Pre-pass, one thread per offset t (0..nseg):
 //   bitmap          bit (off[t] + lead) set (the terminal off[nseg] = n too);
 //   dupflag[q]      4 if two offsets coincide inside portion q (empty segments);
@@ -119,12 +125,12 @@ struct SegStreamArgs {
 //                     chain of dependent loads a per-boundary search over the offsets costs
 //                     (the first version galloped and bisected: ~10 round trips, 12 us).
 // bitmap and dupflag must be zero on entry.
-__global__ void seg_prepare_kernel(const int64_t *off, int64_t nseg, int64_t n, int64_t lead, int64_t P,
-                                   int64_t Q, int64_t *lb, uint32_t *dupflag, uint32_t *bitmap) {
+__global__ void seg_prepare_kernel(const int64_t *off, int64_t ucols, int64_t nseg, int64_t n, int64_t lead,
+                                   int64_t P, int64_t Q, int64_t *lb, uint32_t *dupflag, uint32_t *bitmap) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t > nseg) return;
-    const int64_t e = __ldg(off + t);
-    const int64_t prev = t > 0 ? __ldg(off + t - 1) : -1;
+    const int64_t e = seg_off(off, ucols, t);
+    const int64_t prev = t > 0 ? seg_off(off, ucols, t - 1) : -1;
     const int64_t pos = e + lead;
     const int ps = 63 - __clzll(P);  // P is a power of two (32 KiB of input elements)
     atomicOr(bitmap + (pos >> 5), 1u << (pos & 31));
@@ -146,17 +152,18 @@ __global__ void seg_prepare_kernel(const int64_t *off, int64_t nseg, int64_t n, 
 // exclusive scan keeps the last element in totals[] from before the launch (input and output
 // may alias) and adds it to the last exclusive value.
 template <typename TIn, typename A>
-__global__ void seg_last_in_kernel(const TIn *in, const int64_t *off, int64_t nseg, A *tot) {
+__global__ void seg_last_in_kernel(const TIn *in, const int64_t *off, int64_t ucols, int64_t nseg, A *tot) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nseg) return;
-    const int64_t b = __ldg(off + t), e = __ldg(off + t + 1);
+    const int64_t b = seg_off(off, ucols, t), e = seg_off(off, ucols, t + 1);
     tot[t] = e > b ? (A)in[e - 1] : (A)0;
 }
 template <typename TOut, typename A>
-__global__ void seg_totals_gather_kernel(const TOut *out, const int64_t *off, int64_t nseg, A *tot, int exclusive) {
+__global__ void seg_totals_gather_kernel(const TOut *out, const int64_t *off, int64_t ucols, int64_t nseg, A *tot,
+                                         int exclusive) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nseg) return;
-    const int64_t b = __ldg(off + t), e = __ldg(off + t + 1);
+    const int64_t b = seg_off(off, ucols, t), e = seg_off(off, ucols, t + 1);
     A v = (A)0;
     if (e > b) {
         // one 8-byte element per segment out of a multi-GB array: fetch 64 bytes from DRAM into

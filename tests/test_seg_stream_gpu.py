@@ -174,6 +174,42 @@ def test_full_size_int32_to_int64_one_million_segments(ps_lib):
     assert np.array_equal(tots, want_t)
 
 
+@pytest.mark.parametrize("din,dout,rows,cols", [
+    (np.int32, np.int64, 1 << 17, 250),    # unaligned rows (1000 bytes)
+    (np.int32, np.int64, 1 << 17, 256),    # aligned rows: the rows kernel's domain, below its crossover
+    (np.int32, np.int32, 1 << 16, 501),
+    (np.int64, np.int64, 1 << 16, 250),
+    (np.float32, np.float32, 1 << 17, 250),
+    (np.float64, np.float64, 1 << 16, 127),
+])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_short_rows_of_a_large_batch_run_on_the_region_kernel(ps_lib, seg_kernel, din, dout, rows, cols, exclusive):
+    """ps_scan_batched on many short contiguous rows (>= 32 MiB in all, no seeds): one
+    segmented scan of the flat array with computed offsets on the shared-memory-region
+    kernel; results and row totals against numpy, and against the look-back route."""
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(rows + cols)
+    fl = np.dtype(din).kind == "f"
+    acc = np.float64 if fl else np.int64
+    xh = (r.integers(0, 1024, (rows, cols)) / 1024.0).astype(din) if fl else r.integers(-50, 200, (rows, cols)).astype(din)
+    assert xh.nbytes >= 32 << 20
+    inc = np.cumsum(xh.astype(acc), axis=1)
+    want = ((inc - xh.astype(acc)) if exclusive else inc).astype(dout)
+    x = torch.from_numpy(xh).cuda()
+    res = []
+    for k in (0, 1):
+        seg_kernel(k)
+        out = torch.zeros((rows, cols), dtype=getattr(torch, np.dtype(dout).name), device="cuda")
+        tots = torch.zeros(rows, dtype=getattr(torch, np.dtype(acc).name), device="cuda")
+        device.scan_batched(x, out, exclusive=exclusive, row_totals=tots)
+        torch.cuda.synchronize()
+        got, gt = out.cpu().numpy(), tots.cpu().numpy()
+        assert np.array_equal(got, want), (k, din, rows, cols, exclusive)  # the 2^-10 float grid sums exactly
+        assert np.array_equal(gt, inc[:, -1]), (k, din, rows, cols)
+        res.append(got)
+    assert np.array_equal(res[0], res[1])
+
+
 @pytest.fixture(scope="module")
 def ps_lib():
     if not torch.cuda.is_available():
