@@ -73,6 +73,9 @@ while time.time() < deadline:
     if cases % 7 == 0:  # batched rows: both kernels, row tickets, short rows, per-row tile grids
         rows = int(rng.choice([int(rng.integers(1, 700)), int(rng.integers(700, 20000))]))
         cols = int(rng.choice([int(rng.integers(1, 40000)), int(rng.integers(1, 3000))]))
+        if cases % 21 == 0:  # a large batch of short rows: the flat segmented scan on the region kernel
+            cols = int(rng.integers(1, 700))
+            rows = (40 << 20) // (4 * cols) + int(rng.integers(0, 1000))
         b = rng.integers(0, 255, (rows, cols)).astype(np.int32)
         knobs = {b"rows_kernel": int(rng.integers(0, 3)), b"rows_dynamic": int(rng.integers(0, 2)),
                  b"rows_multi": int(rng.integers(0, 2)), b"tiles_row_lead": int(rng.integers(0, 2))}
