@@ -965,8 +965,13 @@ int ps_scan_batched(const void *in, void *out, int64_t rows, int64_t cols, int64
                                rows * row_bytes >= g_tune.rounds_min_bytes && scratch &&
                                scratch_bytes >= seg_stream_scratch_bytes(rows * cols, (int)dsize(dtype_in)) &&
                                scratch_bytes >= seg_scratch_bytes(rows * cols, (int)dsize(dtype_in));
+    // smaller batches of very short rows: the look-back tiles' uniform-segment scan (0.29-0.31 of
+    // the peak at 2^22 int32 in rows of 64-256 columns, where a row per TMA item gives 0.05-0.18)
+    const bool flat_small = rows > 1 && !row_seeds && ld_in == cols && ld_out == cols && g_tune.rows_kernel != 2 &&
+                            g_tune.tiles_row_lead && row_bytes <= (floats ? 512 : 1024) && scratch &&
+                            scratch_bytes >= seg_scratch_bytes(rows * cols, (int)dsize(dtype_in));
 #define CALL(TI, TO)                                                                                            \
-    if (rows > 1 && !flat_segments && rows_kernel_applies<TI, TO>(in, rows, cols, ld_in))                       \
+    if (rows > 1 && !flat_segments && !flat_small && rows_kernel_applies<TI, TO>(in, rows, cols, ld_in))        \
         return launch_rows<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, row_seeds, row_totals, scratch, \
                                    scratch_bytes, s);                                                           \
     return launch_scan<TI, TO>(in, out, rows, cols, ld_in, ld_out, exclusive, 0, row_seeds, row_seeds ? rows : 0, \

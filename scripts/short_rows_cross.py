@@ -11,10 +11,12 @@ from paper_2312_14874_b200 import _lib, device  # noqa: E402
 
 lib = _lib.load()
 peak = float(json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"])
+REPS = 5 if len(sys.argv) < 2 or int(sys.argv[1]) >= 26 else 50
+LOGN = int(sys.argv[1]) if len(sys.argv) > 1 else 28  # log2 of the batch's elements (4-byte input)
 for din, dout in ((torch.int32, torch.int64), (torch.int64, torch.int64), (torch.float32, torch.float32)):
     es = 4 if din != torch.int64 else 8
     for cols in (64, 128, 256, 512, 1024, 2048, 4096):
-        rows = (1 << (28 if es == 4 else 27)) // cols
+        rows = (1 << (LOGN if es == 4 else LOGN - 1)) // cols
         x = torch.rand((rows, cols), device="cuda").to(din) if din.is_floating_point else torch.randint(0, 256, (rows, cols), dtype=din, device="cuda")
         out = torch.empty((rows, cols), dtype=dout, device="cuda")
         res = []
@@ -26,11 +28,11 @@ for din, dout in ((torch.int32, torch.int64), (torch.int64, torch.int64), (torch
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                for _ in range(5):
+                for _ in range(REPS):
                     device.scan_batched(x, out)
                 b.record()
                 torch.cuda.synchronize()
-                ms = a.elapsed_time(b) / 5
+                ms = a.elapsed_time(b) / REPS
                 res.append(f"{'rows' if rk == 2 else 'segm'} {ms*1e3:7.1f} us ({rows*cols*(x.element_size()+out.element_size())/ms/1e6/peak:.3f})")
             except Exception as e:  # noqa: BLE001
                 res.append(f"{'rows' if rk == 2 else 'segm'} failed: {str(e)[:40]}")
