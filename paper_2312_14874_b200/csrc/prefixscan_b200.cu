@@ -615,17 +615,19 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
     // many short contiguous rows without seeds: one flat segmented scan with uniform
     // segments (a look-back tile per row would leave most of each tile idle)
     if (rows > 1 && g_tune.tiles_row_lead && !seed_terms && seed_bits == 0 && !mail && ld_in == cols && ld_out == cols &&
-        cols * 4 <= TILE && scratch && scratch_bytes >= seg_scratch_bytes(rows * cols, (int)sizeof(TIn))) {
-        // large inputs: the shared-memory-region kernel with computed offsets (one HBM read and
-        // write per element; 2^20 rows x 250 int32 -> int64: 0.31 -> ~0.8 of the peak)
+        scratch) {
+        // large batches, rows of any length that the rows kernel cannot stream (or short ones):
+        // the shared-memory-region kernel with computed offsets -- one HBM read and write per
+        // element (2^20 rows x 250 int32 -> int64: 0.31 -> 0.70 of the peak; 16384 x 16383: 0.80 -> 0.9+)
         if (g_tune.seg_kernel != 1 && rows * cols * (int64_t)sizeof(TIn) >= g_tune.rounds_min_bytes &&
             scratch_bytes >= seg_stream_scratch_bytes(rows * cols, (int)sizeof(TIn))) {
             const int rc = launch_seg_stream<TIn, TOut>(in, out, rows * cols, nullptr, rows, exclusive, totals, scratch,
                                                         scratch_bytes, epoch, s, cols);
             if (rc >= 0) return rc;
         }
-        return launch_segmented<TIn, TOut>(in, out, rows * cols, nullptr, rows, exclusive, totals, scratch, epoch, s,
-                                           cols);
+        if (cols * 4 <= TILE && scratch_bytes >= seg_scratch_bytes(rows * cols, (int)sizeof(TIn)))
+            return launch_segmented<TIn, TOut>(in, out, rows * cols, nullptr, rows, exclusive, totals, scratch, epoch, s,
+                                               cols);
     }
     a.tiles_per_row = (a.lead + max_lead + cols + TILE - 1) / TILE;
     const int64_t tiles = rows * a.tiles_per_row;
@@ -934,7 +936,9 @@ size_t ps_scan_batched_scratch_bytes(int64_t rows, int64_t cols, int dtype_in, i
     if (!pair_ok(dtype_in, dtype_out) || rows < 0 || cols < 0) return 0;
     const int64_t tile = tile_of_dtype(dtype_in);
     size_t need = desc_bytes(rows * ((cols + tile - 1) / tile + 1));
-    if (rows > 1 && cols * 4 <= tile) {  // short rows may run as one segmented scan of the flat array
+    // short rows, and rows the rows kernel cannot stream (byte length not a multiple of 16), may
+    // run as one segmented scan of the flat array
+    if (rows > 1 && (cols * 4 <= tile || (cols * (int64_t)dsize(dtype_in)) % 16 != 0)) {
         const size_t a = seg_scratch_bytes(rows * cols, (int)dsize(dtype_in));
         const size_t b = seg_stream_scratch_bytes(rows * cols, (int)dsize(dtype_in));
         need = std::max(need, std::max(a, b));

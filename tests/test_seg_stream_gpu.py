@@ -181,12 +181,16 @@ def test_full_size_int32_to_int64_one_million_segments(ps_lib):
     (np.int64, np.int64, 1 << 16, 250),
     (np.float32, np.float32, 1 << 17, 250),
     (np.float64, np.float64, 1 << 16, 127),
+    (np.int32, np.int64, 2049, 16383),     # long rows the rows kernel cannot stream (not a multiple of 16 bytes)
+    (np.float32, np.float32, 1500, 20001),
+    (np.int64, np.int64, 700, 30001),
 ])
 @pytest.mark.parametrize("exclusive", [False, True])
 def test_short_rows_of_a_large_batch_run_on_the_region_kernel(ps_lib, seg_kernel, din, dout, rows, cols, exclusive):
-    """ps_scan_batched on many short contiguous rows (>= 32 MiB in all, no seeds): one
-    segmented scan of the flat array with computed offsets on the shared-memory-region
-    kernel; results and row totals against numpy, and against the look-back route."""
+    """ps_scan_batched on contiguous rows without seeds, >= 32 MiB in all -- short rows, and
+    rows of any length whose byte size is not a multiple of 16: one segmented scan of the flat
+    array with computed offsets on the shared-memory-region kernel; results and row totals
+    against numpy, and against the look-back route."""
     from paper_2312_14874_b200 import device
     r = np.random.default_rng(rows + cols)
     fl = np.dtype(din).kind == "f"
