@@ -89,6 +89,7 @@ struct Tuning {
     int64_t round_prefetch = 0;             // bulk L2 prefetch of each reducer portion (1 = on)
     int rows_kernel = 0;                    // batched: 0 auto, 1 look-back tiles, 2 one CTA per row
     int stream_inflight = 2;                // stream kernel: regions' TMA loads outstanding per SM (0 = ring)
+    int stream_copy_in = 1;                 // stream kernel for in/out pairs at different 32-byte phases (0: look-back tiles)
     int rows_dynamic = 1;                   // rows kernel: rows from a grid-wide ticket (0 = fixed shares)
     int reduce_blocks = 1;                  // ps_reduce: blocks from a ticket (0 = grid-stride shares)
     int add_chunked = 1;                    // ps_add_offset: one CTA per 64 KiB (0 = grid-stride shares)
@@ -281,7 +282,7 @@ int stream_grid() {
 template <typename TIn, typename TOut>
 int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclusive, uint64_t seed_bits,
                   const void *seed_terms, int64_t n_seed_terms, void *total, void *scratch, size_t scratch_bytes,
-                  uint32_t epoch, cudaStream_t s, const Mailbox *mail = nullptr) {
+                  uint32_t epoch, cudaStream_t s, const Mailbox *mail = nullptr, bool copy_in = false) {
     const int64_t G = stream_grid<TIn, TOut>();
     if (G <= 0 || G > STREAM_MAX_GRID) return PS_ERR_CUDA_BASE + (int)cudaErrorLaunchFailure;
     const int64_t P = stream_portion<TIn, TOut>();
@@ -304,6 +305,7 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
     a.epoch = epoch;
     a.exclusive = exclusive;
     a.inflight = g_tune.stream_inflight;
+    a.copy_in = copy_in ? 1 : 0;
     void *params[] = {&a};
     const void *kern = (const void *)SKERN;
     if (a.stall.max_ns) {  // stress-test instantiation with the stall sites compiled in
@@ -609,6 +611,24 @@ int launch_scan(const void *in, void *out, int64_t rows, int64_t cols, int64_t l
         (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big && stream_grid<TIn, TOut>() <= STREAM_MAX_GRID)))
         return launch_stream<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
                                         scratch, scratch_bytes, epoch, s, mail);
+    // in/out pairs at different 32-byte phases: the output decides the tile grid (256-bit
+    // stores); the input is bulk-copied if some lead of that grid leaves it 16-byte aligned,
+    // otherwise the producer warp copies it (stream_kernel.cuh, copy_in)
+    if (rows == 1 && !vec && g_tune.stream_copy_in && (uintptr_t)in % sizeof(TIn) == 0 && (uintptr_t)out % sizeof(TOut) == 0 &&
+        (g_tune.scan_kernel == 3 || (g_tune.scan_kernel == 0 && big && stream_grid<TIn, TOut>() <= STREAM_MAX_GRID))) {
+        const int64_t ev_out = 32 / (int64_t)sizeof(TOut), vec_in = 32 / (int64_t)sizeof(TIn);
+        const int64_t k = (int64_t)(((uintptr_t)out % 32) / sizeof(TOut));  // lead = k (mod ev_out)
+        int64_t pick = k;
+        bool tma = false;
+        for (int64_t l = k; l < vec_in; l += ev_out)
+            if (((uintptr_t)in - (uintptr_t)(l * (int64_t)sizeof(TIn))) % 16 == 0) {
+                pick = l;
+                tma = true;
+                break;
+            }
+        return launch_stream<TIn, TOut>(in, out, cols, pick, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
+                                        scratch, scratch_bytes, epoch, s, mail, !tma);
+    }
     if (rows == 1 && vec && g_tune.scan_kernel == 2)
         return launch_rounds<TIn, TOut>(in, out, cols, a.lead, exclusive, seed_bits, seed_terms, n_seed_terms, totals,
                                         scratch, scratch_bytes, epoch, s, mail);
@@ -839,6 +859,9 @@ int ps_set_tuning(const char *key, int64_t value) {
     } else if (!std::strcmp(key, "rows_kernel")) {
         if (value < 0 || value > 2) return PS_ERR_ARG;
         g_tune.rows_kernel = (int)value;
+    } else if (!std::strcmp(key, "stream_copy_in")) {
+        if (value < 0 || value > 1) return PS_ERR_ARG;
+        g_tune.stream_copy_in = (int)value;
     } else if (!std::strcmp(key, "stream_inflight")) {
         if (value < 0 || value > 8) return PS_ERR_ARG;
         g_tune.stream_inflight = (int)value;
@@ -900,6 +923,7 @@ int64_t ps_get_tuning(const char *key) {
     if (!std::strcmp(key, "round_prefetch")) return g_tune.round_prefetch;
     if (!std::strcmp(key, "rows_kernel")) return g_tune.rows_kernel;
     if (!std::strcmp(key, "select_kernel")) return g_select_kernel;
+    if (!std::strcmp(key, "stream_copy_in")) return g_tune.stream_copy_in;
     if (!std::strcmp(key, "stream_inflight")) return g_tune.stream_inflight;
     if (!std::strcmp(key, "rows_dynamic")) return g_tune.rows_dynamic;
     if (!std::strcmp(key, "rows_multi")) return g_tune.rows_multi;

@@ -41,6 +41,7 @@ struct StreamArgs {
     uint32_t epoch;
     int exclusive;
     int inflight;      // producer: at most this many regions' loads outstanding (0: NBUF)
+    int copy_in;       // 1: the producer warp copies portions with element-sized loads (input not TMA-alignable)
     Stall stall;       // stress tests: stall injection at every role hand-off
     Mailbox mail;      // seed += totals published by the ranks before this one
 };
@@ -253,6 +254,56 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
 
     if (warp == W_PROD) {
         // ============================ producer ===================================
+        if (a.copy_in) {
+            // The output's 32-byte phase fixes the tile grid (256-bit stores); an input whose
+            // 16-byte phase does not fit that grid cannot be bulk-copied, so the whole producer
+            // warp copies each portion with element-sized streaming loads into the same
+            // shared-memory layout -- reducers and scanners do not notice.  (Before: such
+            // in/out pairs fell back to the look-back tiles with scalar accesses, 0.49 of peak.)
+            // cp.async (LDGSTS) of one element per lane: no registers held, three regions'
+            // copies in flight per SM (a load/store loop of one warp moved a sixth of the rate)
+            constexpr int D = 3;
+            auto issue = [&](int64_t r) {
+                if (whole(r)) {
+                    const TIn *src = in + p0_of(r);
+                    const uint32_t dst = smem_addr(buf + (size_t)(r % NBUF) * P);
+                    if (sizeof(TIn) == 4 && (reinterpret_cast<uintptr_t>(in) & 7) == 0) {
+                        // 4-byte elements on an 8-byte boundary: two per copy, half the instructions
+#pragma unroll 8
+                        for (int64_t i = 2 * lane; i < P; i += 64)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + (uint32_t)(i * sizeof(TIn))),
+                                         "l"(src + i)
+                                         : "memory");
+                    } else {
+#pragma unroll 8
+                        for (int64_t i = lane; i < P; i += 32)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + (uint32_t)(i * sizeof(TIn))),
+                                         "l"(src + i), "n"(sizeof(TIn))
+                                         : "memory");
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            for (int64_t r = 0; r < a.rounds; ++r) {
+                const int b = (int)(r % NBUF);
+                if (lane == 0) {
+                    stall_site<STALL>(a.stall, r * G + c, 0, 1);
+                    if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
+                }
+                __syncwarp();
+                issue(r);
+                if (r >= D - 1) {
+                    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[(r - (D - 1)) % NBUF]);
+                }
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                for (int64_t r = a.rounds > D - 1 ? a.rounds - (D - 1) : 0; r < a.rounds; ++r) mbar_arrive(&full[r % NBUF]);
+            return;
+        }
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             for (int64_t r = 0; r < a.rounds; ++r) {

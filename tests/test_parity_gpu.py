@@ -854,6 +854,30 @@ def test_cfg5_baseline_draw_bit_exact(ps):
     assert res["bit_exact"] and res["total"] == 1073746006907
 
 
+@pytest.mark.parametrize("din,dout", [(np.int32, np.int64), (np.int64, np.int64), (np.float32, np.float32)])
+def test_stream_kernel_input_and_output_at_different_phases(ps, din, dout):
+    """Inputs >= 32 MiB whose input and output sit at different 32-byte phases run on the stream
+    kernel with the tile grid aligned to the OUTPUT: bulk copies where the input's 16-byte phase
+    fits, the producer warp's element-wise cp.async otherwise.  Every element-offset pair."""
+    from paper_2312_14874_b200 import device
+    r = np.random.default_rng(41)
+    n = (9 << 20) + 4321 if np.dtype(din).itemsize == 4 else (5 << 20) + 99
+    fl = np.dtype(din).kind == "f"
+    acc = np.float64 if fl else np.int64
+    xh = (r.integers(0, 1024, n + 8) / 1024.0).astype(din) if fl else r.integers(-100, 300, n + 8).astype(din)
+    xd = torch.from_numpy(xh).cuda()
+    od = torch.empty(n + 8, dtype=getattr(torch, np.dtype(dout).name), device="cuda")
+    for oi, oo in ((0, 1), (1, 0), (3, 2), (5, 0), (2, 7), (7, 7), (4, 1)):
+        excl = bool((oi + oo) & 1)
+        o = od[oo:oo + n]
+        o.zero_()
+        tot = device.scan(xd[oi:oi + n], o, exclusive=excl, seed=3)
+        c = np.cumsum(xh[oi:oi + n].astype(acc)) + acc(3)
+        want = (np.concatenate([[acc(3)], c[:-1]]) if excl else c).astype(dout)  # exact on the 2^-10 grid
+        assert np.array_equal(o.cpu().numpy(), want), (din, oi, oo, excl)
+        assert tot.cpu().numpy().view(acc)[0] == c[-1]
+
+
 def test_cuda_graph_replays(ps):
     """Scans captured in a CUDA graph and replayed several times over changing input
     contents: every replay starts from a zeroed scratch (the epochs are baked into the
