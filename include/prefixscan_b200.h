@@ -40,6 +40,14 @@
  *   entry point in turn: the non-descriptor words kernels leave in it
  *   (segment and compaction bookkeeping) keep their two low bits 0, so they
  *   never pass for a published descriptor of a later epoch.
+ * - Forward progress.  The persistent kernels (stream, rows, CSR regions, single-pass select)
+ *   are cooperative launches of at most one resident grid, so every CTA a role waits on is
+ *   running.  The look-back tiles kernels (small inputs) take tile ids from blockIdx and rely
+ *   on the hardware dispatching CTAs in increasing linear order: a tile only ever waits on
+ *   lower-numbered tiles, which are resident or finished by then -- the argument CUB's
+ *   single-pass scan rests on; there is no atomic tile counter.  Cross-GPU waits
+ *   (ps_scan_mailbox) give up after ~10 s and raise the caller's timeout flag instead of
+ *   hanging.
  * - `in == out` (in place) is allowed; partial overlap is not.
  * - Return 0 on success, a PS_ERR_* (>0) on misuse, or a cudaError_t value
  *   offset by PS_ERR_CUDA_BASE on a CUDA failure.
