@@ -290,7 +290,7 @@ int ps_scan_batched_host(const void *in_host, void *out_host, int64_t rows, int6
  *   "stream_copy_in"   1-D inputs whose input and output sit at different 32-byte phases:
  *                      1 = stream kernel with the tile grid aligned to the output (bulk copies
  *                      where the input's 16-byte phase fits, element-wise cp.async by the
- *                      producer warp otherwise), 0 = look-back tiles (default 1)
+ *                      reducer warps otherwise), 0 = look-back tiles (default 1)
  *   "rows_dynamic"     rows kernel: 1 = rows handed out from a grid-wide ticket kept in
  *                      the scratch's control words (faster SMs take more rows),
  *                      0 = CTA c takes rows c, c+G, ... (default 1)

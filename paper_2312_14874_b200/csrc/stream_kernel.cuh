@@ -25,6 +25,10 @@
 
 #include "rounds_kernel.cuh"
 
+#ifndef PS_COPY_DEPTH  // copy_in: regions whose element-wise copies are in flight per reducer warp
+#define PS_COPY_DEPTH 3
+#endif
+
 namespace ps {
 
 struct StreamArgs {
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
 
     if (tid == 0) {
         for (int b = 0; b < NBUF; ++b) {
-            mbar_init(&full[b], 1);
+            mbar_init(&full[b], a.copy_in ? RWP : 1);  // copy_in: every reducer warp lands its own chunks
             mbar_init(&red[b], 1);
             mbar_init(&pre[b], 1);
             mbar_init(&freeb[b], SW);
@@ -254,56 +258,7 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
 
     if (warp == W_PROD) {
         // ============================ producer ===================================
-        if (a.copy_in) {
-            // The output's 32-byte phase fixes the tile grid (256-bit stores); an input whose
-            // 16-byte phase does not fit that grid cannot be bulk-copied, so the whole producer
-            // warp copies each portion with element-sized streaming loads into the same
-            // shared-memory layout -- reducers and scanners do not notice.  (Before: such
-            // in/out pairs fell back to the look-back tiles with scalar accesses, 0.49 of peak.)
-            // cp.async (LDGSTS) of one element per lane: no registers held, three regions'
-            // copies in flight per SM (a load/store loop of one warp moved a sixth of the rate)
-            constexpr int D = 3;
-            auto issue = [&](int64_t r) {
-                if (whole(r)) {
-                    const TIn *src = in + p0_of(r);
-                    const uint32_t dst = smem_addr(buf + (size_t)(r % NBUF) * P);
-                    if (sizeof(TIn) == 4 && (reinterpret_cast<uintptr_t>(in) & 7) == 0) {
-                        // 4-byte elements on an 8-byte boundary: two per copy, half the instructions
-#pragma unroll 8
-                        for (int64_t i = 2 * lane; i < P; i += 64)
-                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + (uint32_t)(i * sizeof(TIn))),
-                                         "l"(src + i)
-                                         : "memory");
-                    } else {
-#pragma unroll 8
-                        for (int64_t i = lane; i < P; i += 32)
-                            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + (uint32_t)(i * sizeof(TIn))),
-                                         "l"(src + i), "n"(sizeof(TIn))
-                                         : "memory");
-                    }
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            };
-            for (int64_t r = 0; r < a.rounds; ++r) {
-                const int b = (int)(r % NBUF);
-                if (lane == 0) {
-                    stall_site<STALL>(a.stall, r * G + c, 0, 1);
-                    if (r >= NBUF) mbar_wait(&freeb[b], par(r - NBUF));
-                }
-                __syncwarp();
-                issue(r);
-                if (r >= D - 1) {
-                    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&full[(r - (D - 1)) % NBUF]);
-                }
-            }
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncwarp();
-            if (lane == 0)
-                for (int64_t r = a.rounds > D - 1 ? a.rounds - (D - 1) : 0; r < a.rounds; ++r) mbar_arrive(&full[r % NBUF]);
-            return;
-        }
+        if (a.copy_in) return;  // no bulk copies: the reducer warps fetch their own chunks (below)
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             for (int64_t r = 0; r < a.rounds; ++r) {
@@ -337,8 +292,42 @@ __global__ void __launch_bounds__((SW + RWP + 2) * 32, MINB) scan_stream_kernel(
     if (warp >= SW && warp < W_PROD) {
         // ============================ reducers ===================================
         const int rw = warp - SW;
+        // copy_in.  The output's 32-byte phase fixes the tile grid (256-bit stores); an input
+        // whose 16-byte phase does not fit that grid cannot be bulk-copied.  Each reducer warp
+        // then fetches its own chunks of a portion with element-wise cp.async (LDGSTS: no
+        // registers held), D - 1 regions ahead of the one it reduces, into the very layout a
+        // bulk copy would leave -- scanners and ledger do not notice.  (Before: such in/out
+        // pairs ran on the look-back tiles with scalar accesses, 0.31-0.50 of the peak; one
+        // copying warp per SM reached 0.5, its copies in flight being too few.)
+        constexpr int D = PS_COPY_DEPTH;
+        auto copy_stage = [&](int64_t q) {
+            if (q < a.rounds) {
+                if (lane == 0 && q >= NBUF) mbar_wait(&freeb[q % NBUF], par(q - NBUF));
+                __syncwarp();
+                if (whole(q)) {
+                    const TIn *src = in + p0_of(q);
+                    const uint32_t dst = smem_addr(buf + (size_t)(q % NBUF) * P);
+                    for (int64_t ch = rw; ch < nchunk; ch += RWP) {
+#pragma unroll 8
+                        for (int64_t i = ch * CHUNK + lane; i < (ch + 1) * CHUNK; i += 32)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + (uint32_t)(i * sizeof(TIn))),
+                                         "l"(src + i), "n"(sizeof(TIn))
+                                         : "memory");
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (a.copy_in)
+            for (int64_t q = 0; q < D - 1; ++q) copy_stage(q);
         for (int64_t r = 0; r < a.rounds; ++r) {
             const int b = (int)(r % NBUF);
+            if (a.copy_in) {
+                copy_stage(r + D - 1);
+                asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");  // region r's copies have landed
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[b]);
+            }
             mbar_wait(&full[b], par(r));
 #ifdef PS_TRACE
                 if (g_trace && rw == 0 && lane == 0) g_trace[(r * G + c) * 8 + 1] = gtimer();

@@ -8,6 +8,10 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+if len(sys.argv) > 1 and sys.argv[1].endswith(".so"):  # a variant build
+    from paper_2312_14874_b200 import _build  # noqa: E402
+    _build.LIB_PATH = sys.argv[1]
+    _build.up_to_date = lambda: True
 from paper_2312_14874_b200 import _lib, device  # noqa: E402
 
 lib = _lib.load()

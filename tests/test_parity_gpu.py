@@ -858,7 +858,7 @@ def test_cfg5_baseline_draw_bit_exact(ps):
 def test_stream_kernel_input_and_output_at_different_phases(ps, din, dout):
     """Inputs >= 32 MiB whose input and output sit at different 32-byte phases run on the stream
     kernel with the tile grid aligned to the OUTPUT: bulk copies where the input's 16-byte phase
-    fits, the producer warp's element-wise cp.async otherwise.  Every element-offset pair."""
+    fits, the reducer warps' element-wise cp.async otherwise.  A spread of element-offset pairs."""
     from paper_2312_14874_b200 import device
     r = np.random.default_rng(41)
     n = (9 << 20) + 4321 if np.dtype(din).itemsize == 4 else (5 << 20) + 99
