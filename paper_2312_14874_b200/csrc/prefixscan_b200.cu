@@ -343,8 +343,14 @@ int launch_stream(const void *in, void *out, int64_t n, int64_t lead, int exclus
 #define PS_SEG_RWP 4
 #endif
 constexpr int GSW = PS_SEG_SW, GROWS = PS_SEG_ROWS, GNBUF = PS_SEG_NBUF, GRWP = PS_SEG_RWP;
-#define GGEO SegStreamGeom<TIn, GSW, GROWS, GNBUF, GRWP>
-#define GKERN seg_stream_kernel<TIn, TOut, GSW, GROWS, GNBUF, GRWP>
+// 8-byte integer inputs: a 32-lane row is half the bytes of a 4-byte one for the same reducer
+// work, and the reducers set the region rate -- eight reducer warps instead of four
+// (2^27 int64, 16K / 1M segments: 424 / 540 -> 395 / 509 us; 4-byte and float inputs: +-0)
+template <typename TIn> struct SegCfg { static constexpr int RWP = GRWP; };
+template <> struct SegCfg<int64_t> { static constexpr int RWP = GRWP == 4 ? 8 : GRWP; };
+template <> struct SegCfg<uint64_t> { static constexpr int RWP = GRWP == 4 ? 8 : GRWP; };
+#define GGEO SegStreamGeom<TIn, GSW, GROWS, GNBUF, SegCfg<TIn>::RWP>
+#define GKERN seg_stream_kernel<TIn, TOut, GSW, GROWS, GNBUF, SegCfg<TIn>::RWP>
 constexpr int64_t SEG_STREAM_MAX_GRID = STREAM_MAX_GRID;
 
 template <typename TIn, typename TOut>
